@@ -1,0 +1,120 @@
+"""CPU: the C-ABI library builds, loads and exports what the header declares;
+host-side packing mirrors the reference's per-request reads."""
+
+from __future__ import annotations
+
+import re
+import subprocess
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from conftest import REPO
+from paper_2504_03887_b200 import _native
+from paper_2504_03887_b200.allocator import (AllocatorConfig, pack_trace,
+                                             round_request, segment_size_for)
+from paper_2504_03887_b200.errors import ZeroSize
+
+MIB = 1 << 20
+HEADER = REPO / "include" / "peakmem_b200.h"
+
+
+def header_functions():
+    text = HEADER.read_text()
+    return sorted(set(re.findall(r"^\s*(?:int|const char\*)\s+(pm_\w+)\(",
+                                 text, re.M)))
+
+
+def test_header_declares_what_python_binds():
+    assert header_functions() == sorted(_native.EXPORTED_SYMBOLS)
+
+
+def test_library_exports_every_declared_symbol():
+    lib = _native.LIB_PATH
+    if not lib.exists():
+        import __graft_entry__
+        __graft_entry__.build()
+    out = subprocess.run(["nm", "-D", "--defined-only", str(lib)],
+                         capture_output=True, text=True, check=True).stdout
+    exported = set(re.findall(r"\bT (pm_\w+)", out))
+    for sym in header_functions():
+        assert sym in exported, sym
+    loaded = _native.load_library()
+    assert loaded.pm_version() == 1
+
+
+def test_library_is_sm100a():
+    out = subprocess.run(["cuobjdump", "--list-elf", str(_native.LIB_PATH)],
+                         capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_workspace_sizing_is_host_only():
+    small = _native.workspace_bytes(1000, 100, 10)
+    big = _native.workspace_bytes(10_000, 100, 10)
+    assert big - small >= 16 * 9000 - 256  # 16 B record per request
+
+
+def test_struct_layouts_match_header():
+    assert _native.REQ_DTYPE.itemsize == 16
+    assert _native.CFG_DTYPE.itemsize == 64
+    assert _native.RESULT_DTYPE.itemsize == 64
+
+
+# --- host-side arithmetic and packing (reference: allocator.py:49-92) -----
+
+@pytest.mark.parametrize("size,expected", [(1, 512), (512, 512), (513, 1024),
+                                           (511, 512), (1024, 1024), (4097, 4608)])
+def test_round_request(size, expected):
+    assert round_request(size) == expected
+
+
+def test_round_request_zero():
+    with pytest.raises(ZeroSize):
+        round_request(0)
+
+
+def test_segment_table():
+    table = {1: 2 * MIB, 512: 2 * MIB, MIB: 2 * MIB, MIB + 1: 20 * MIB,
+             10 * MIB: 20 * MIB, 10 * MIB + 1: 12 * MIB, 11 * MIB: 12 * MIB,
+             64 * MIB: 64 * MIB}
+    cfg = AllocatorConfig()
+    assert {s: segment_size_for(round_request(s), cfg) for s in table} == table
+
+
+def test_config_validation():
+    with pytest.raises(ValueError):
+        AllocatorConfig(alignment=500)
+    with pytest.raises(ValueError):
+        AllocatorConfig(max_split_size=8 * MIB)
+    assert AllocatorConfig(max_split_size=20 * MIB).max_split_size == 20 * MIB
+
+
+def test_pack_interns_ids_and_streams():
+    p = pack_trace([
+        {"seq_no": 5, "kind": "ALLOC", "block_id": "x", "size": 10, "stream": 7},
+        {"seq_no": 6, "kind": "alloc", "block_id": ("t", 1), "size": 3},
+        {"seq_no": 7, "kind": "free", "block_id": "x"},
+        {"seq_no": 8, "kind": "resize", "block_id": "x"},
+        {"seq_no": 9, "kind": "alloc", "block_id": "y"},
+    ])
+    assert p.seq_nos == [5, 6, 7, 8, 9]
+    assert list(p.reqs["handle"][:3]) == [0, 1, 0]
+    ks = p.reqs["kind_stream"]
+    assert ks[0] & 3 == _native.KIND_ALLOC and ks[0] >> 2 == 0
+    assert ks[1] >> 2 == 1           # stream 0 interned after stream 7
+    assert ks[2] & 3 == _native.KIND_FREE
+    assert ks[3] & 3 == _native.KIND_UNKNOWN and p.kinds_raw[3] == "resize"
+    assert ks[4] & 3 == _native.KIND_MISSING
+    assert isinstance(p.host_errors[4], KeyError)
+
+
+def test_engine_refuses_without_gpu(monkeypatch):
+    torch = pytest.importorskip("torch")
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    from paper_2504_03887_b200 import replay
+    from paper_2504_03887_b200.errors import EngineUnavailable
+    with pytest.raises(EngineUnavailable):
+        replay([{"seq_no": 0, "kind": "alloc", "block_id": 1, "size": 512}])
