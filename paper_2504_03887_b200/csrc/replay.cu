@@ -107,8 +107,9 @@ __device__ __forceinline__ void pool_remove_lane(u64* pa, u64* pk, int s,
 // above max_split, largest first (ties: creation order == ascending base),
 // stopping as soon as the new segment fits; stage 2 releases every
 // wholly-free segment.
-__device__ __noinline__ void make_room(WarpState& w, u64* pa, u64* pk,
-                                       long long seg, const Cfg& c, int lane) {
+__device__ __forceinline__ void make_room(WarpState& w, u64* pa, u64* pk,
+                                          long long seg, const Cfg& c,
+                                          int lane) {
   if (c.max_split >= 0) {
     while (w.reserved + seg > c.capacity) {
       u64 bk = ~0ull, ba = ~0ull;
@@ -264,14 +265,32 @@ __device__ __forceinline__ void replay_trace(
             // rounded <= size < rounded + max_split
             u64 bk = ~0ull, ba = ~0ull;
             int bs = -1;
-            for (int s = lane; s < w.F; s += 32) {
-              const u64 k = pk[s] & kKeyMask;
+            const int F = w.F;
+            int s0 = lane;
+            for (; s0 + 96 < F; s0 += 128) {
+              u64 k4[4];
+#pragma unroll
+              for (int u = 0; u < 4; ++u) k4[u] = pk[s0 + 32 * u] & kKeyMask;
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                if (k4[u] - lo < span) {
+                  const u64 a = pa[s0 + 32 * u];
+                  if (k4[u] < bk || (k4[u] == bk && a < ba)) {
+                    bk = k4[u];
+                    ba = a;
+                    bs = s0 + 32 * u;
+                  }
+                }
+              }
+            }
+            for (; s0 < F; s0 += 32) {
+              const u64 k = pk[s0] & kKeyMask;
               if (k - lo < span) {
-                const u64 a = pa[s];
+                const u64 a = pa[s0];
                 if (k < bk || (k == bk && a < ba)) {
                   bk = k;
                   ba = a;
-                  bs = s;
+                  bs = s0;
                 }
               }
             }
@@ -362,10 +381,25 @@ __device__ __forceinline__ void replay_trace(
           w.allocated -= (long long)S;
           const u64 endA = A + S;
           int ns = -1, ps = -1;
-          for (int s = lane; s < w.F; s += 32) {
-            const u64 a = pa[s];
-            if (!fe && a == endA) ns = s;
-            if (!fs && a + (pk[s] & kSizeMask) == A) ps = s;
+          const int F = w.F;
+          int s0 = lane;
+          for (; s0 + 96 < F; s0 += 128) {
+            u64 a4[4], k4[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              a4[u] = pa[s0 + 32 * u];
+              k4[u] = pk[s0 + 32 * u];
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              if (!fe && a4[u] == endA) ns = s0 + 32 * u;
+              if (!fs && a4[u] + (k4[u] & kSizeMask) == A) ps = s0 + 32 * u;
+            }
+          }
+          for (; s0 < F; s0 += 32) {
+            const u64 a = pa[s0];
+            if (!fe && a == endA) ns = s0;
+            if (!fs && a + (pk[s0] & kSizeMask) == A) ps = s0;
           }
           const unsigned bn = __ballot_sync(kFull, ns >= 0);
           const unsigned bp = __ballot_sync(kFull, ps >= 0);
@@ -730,6 +764,24 @@ int pm_replay_host(const pm_req_t* reqs, const int64_t* trace_offsets,
   const size_t b_tl = timeline ? align_up(16 * (size_t)(total > 0 ? total : 1), 256) : 0;
   const size_t bytes =
       b_reqs + b_offs + b_cfgs + b_cfgof + b_order + b_res + b_tl + L.total;
+  {
+    // keep the stream-ordered pool's memory mapped between calls: the
+    // default release threshold (0) unmaps it at every synchronisation
+    static std::mutex mu;
+    static int tuned_dev = -1;
+    int dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess) {
+      std::lock_guard<std::mutex> g(mu);
+      if (tuned_dev != dev) {
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+          uint64_t thr = UINT64_MAX;
+          cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+        tuned_dev = dev;
+      }
+    }
+  }
   void* dmem = nullptr;
   cudaError_t e = cudaMallocAsync(&dmem, bytes, stream);
   if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync");
