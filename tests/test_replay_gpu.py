@@ -308,3 +308,21 @@ def test_replay_batch_api():
     for t, o in zip(traces, outs):
         single = replay(t, AllocatorConfig(device_capacity=64 * MIB))
         assert o.timeline == single.timeline and o.oom_seq_no == single.oom_seq_no
+
+
+def test_many_traces_per_warp_vs_oracle(monkeypatch):
+    # persistent warps replay trace after trace: cap the grid so every warp
+    # handles several traces (state must not leak between them)
+    monkeypatch.setenv("PM_MAX_GRID", "3")
+    reqs, offs = synth.generate(12, first=500)
+    cfg = cfg_record(AllocatorConfig())
+    got, tl = _native.replay_host(reqs, offs, cfg, None, True)
+    want, tl_ref = oracle.replay_batch(reqs, offs, cfg, timeline=True)
+    assert_same(got, want)
+    assert (tl == tl_ref).all()
+    cases = corpus("corpus_seed1000")[:300]
+    r2, o2, c2, f2, _ = pack_corpus(cases)
+    got, tl = _native.replay_host(r2, o2, c2, f2, True)
+    want, tl_ref = oracle.replay_batch(r2, o2, c2, f2, timeline=True)
+    assert_same(got, want)
+    assert (tl == tl_ref).all()
