@@ -29,20 +29,12 @@ int cuda_fail(cudaError_t e, const char* where) {
   return fail(PM_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
 }
 
-constexpr int kDefaultBuckets = 32;  // shared-memory buckets per warp
-constexpr int kWarps = 1;            // warps (traces in flight) per CTA
+constexpr int kWarps = 12;
+constexpr size_t kBucket_host = 32;  // warps (traces in flight) per CTA, 1 CTA / SM
 constexpr int kRetryWarps = 1;
 constexpr int kMaxRetryWarps = 64;
 
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
-
-int buckets_setting() {
-  const char* env = getenv("PM_POOL_BUCKETS");
-  int nb = env ? atoi(env) : kDefaultBuckets;
-  if (nb < 4) nb = 4;
-  if (nb > 32) nb = 32;  // the register directory holds one bucket per lane
-  return nb;
-}
 
 // workspace = ctl | retry list | retry pools | record table
 struct Layout {
@@ -56,7 +48,7 @@ Layout layout_for(int64_t total_events, int64_t max_trace_events,
   Layout L;
   size_t off = align_up(sizeof(pmb::Ctl), 256);
   L.retry_list = off;
-  off = align_up(off + sizeof(int32_t) * (size_t)(n_traces > 0 ? n_traces : 1),
+  off = align_up(off + 2 * sizeof(int32_t) * (size_t)(n_traces > 0 ? n_traces : 1),
                  256);
   const int64_t mx = max_trace_events > 0 ? max_trace_events : 1;
   L.nbmax_g = (int)(mx / 8 + 4);
@@ -72,10 +64,35 @@ Layout layout_for(int64_t total_events, int64_t max_trace_events,
 }
 
 struct Occupancy {
-  int sms = 0, per_sm = 0, nbmax = 0;
+  int sms = 0, per_sm = 0, buckets = 0, warps = 0;
   size_t smem = 0;
+  int per_sm1 = 0;  // tier-1 retry kernel
+  size_t smem1 = 0;
 };
 
+constexpr int kTier1Warps = 8;  // tier 1: a dedicated 32-bucket pool per warp
+
+template <int W>
+int setup_kernel(int optin, int cap, int* buckets, size_t* smem, int* per_sm) {
+  int b = (int)(((size_t)optin - (size_t)W * 32 * 24 - 256) / (kBucket_host * 24));
+  if (cap > 0 && cap < b) b = cap;
+  if (b < 2 * W) b = 2 * W;
+  *buckets = b;
+  *smem = pmb::smem_cta_bytes(b, W);
+  cudaError_t e = cudaFuncSetAttribute(
+      pmb::replay_smem_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      (int)*smem);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+      per_sm, pmb::replay_smem_kernel<W>, W * 32, *smem);
+  if (e != cudaSuccess) return cuda_fail(e, "occupancy");
+  if (*per_sm < 1) return fail(PM_ERR_CUDA, "replay kernel cannot be resident");
+  return PM_SUCCESS;
+}
+
+// Main pass: one CTA of `warps` warps per SM sharing a bucket pool sized to
+// the remaining shared memory (PM_POOL_BUCKETS caps it, PM_REPLAY_WARPS picks
+// 12 or 16 warps; 12 measured faster on C3).  Tier 1: 8 warps x 32 dedicated buckets.
 int query_occupancy(Occupancy* out) {
   static std::mutex mu;
   static int cached_dev = -1;
@@ -88,16 +105,26 @@ int query_occupancy(Occupancy* out) {
     Occupancy o;
     e = cudaDeviceGetAttribute(&o.sms, cudaDevAttrMultiProcessorCount, dev);
     if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceGetAttribute");
-    o.nbmax = buckets_setting();
-    o.smem = (size_t)kWarps * pmb::smem_warp_bytes(o.nbmax);
-    e = cudaFuncSetAttribute(pmb::replay_smem_kernel<kWarps>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)o.smem);
-    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-        &o.per_sm, pmb::replay_smem_kernel<kWarps>, kWarps * 32, o.smem);
-    if (e != cudaSuccess) return cuda_fail(e, "occupancy");
-    if (o.per_sm < 1) o.per_sm = 1;
+    int optin = 0;
+    e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin,
+                               dev);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceGetAttribute");
+    int cap = 0;
+    if (const char* env = getenv("PM_POOL_BUCKETS")) cap = atoi(env);
+    o.warps = kWarps;
+    if (const char* env = getenv("PM_REPLAY_WARPS")) o.warps = atoi(env);
+    int rc;
+    if (o.warps == 12)
+      rc = setup_kernel<12>(optin, cap, &o.buckets, &o.smem, &o.per_sm);
+    else {
+      o.warps = 16;
+      rc = setup_kernel<16>(optin, cap, &o.buckets, &o.smem, &o.per_sm);
+    }
+    if (rc != PM_SUCCESS) return rc;
+    int b1 = 0;
+    rc = setup_kernel<kTier1Warps>(optin, kTier1Warps * 32, &b1, &o.smem1,
+                                   &o.per_sm1);
+    if (rc != PM_SUCCESS) return rc;
     cached = o;
     cached_dev = dev;
   }
@@ -180,23 +207,41 @@ int pm_replay_batch(const pm_req_t* reqs, const int64_t* trace_offsets,
 
   cudaError_t e = cudaMemsetAsync(ctl, 0, sizeof(pmb::Ctl), stream);
   if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync");
-  long long want = ((long long)n_traces + kWarps - 1) / kWarps;
+  int32_t* list1 = retry_list;
+  int32_t* list2 = retry_list + n_traces;
+  long long want = ((long long)n_traces + occ.warps - 1) / occ.warps;
   long long grid = (long long)occ.per_sm * occ.sms;
   if (want < grid) grid = want;
   if (const char* cap = getenv("PM_MAX_GRID")) {  // debugging aid
     const long long g = atoll(cap);
     if (g > 0 && g < grid) grid = g;
   }
-  pmb::replay_smem_kernel<kWarps>
-      <<<(unsigned)grid, kWarps * 32, occ.smem, stream>>>(
-          reqs, trace_offsets, n_traces, cfgs, cfg_of_trace, trace_order,
-          results, timeline, recs, ctl, retry_list, occ.nbmax);
+#define PM_LAUNCH_MAIN(W)                                                     \
+  pmb::replay_smem_kernel<W><<<(unsigned)grid, W * 32, occ.smem, stream>>>(  \
+      reqs, trace_offsets, cfgs, cfg_of_trace, results, timeline, recs, ctl, \
+      0, trace_order, n_traces, list1, occ.buckets)
+  if (occ.warps == 12)
+    PM_LAUNCH_MAIN(12);
+  else
+    PM_LAUNCH_MAIN(16);
+#undef PM_LAUNCH_MAIN
   e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "replay_smem_kernel launch");
+  // tier 1: dedicated 32-bucket pools (grid sized for the worst case; idle
+  // CTAs exit at once when nothing overflowed)
+  long long grid1 = (long long)occ.per_sm1 * occ.sms;
+  long long want1 = ((long long)n_traces + kTier1Warps - 1) / kTier1Warps;
+  if (want1 < grid1) grid1 = want1;
+  pmb::replay_smem_kernel<kTier1Warps>
+      <<<(unsigned)grid1, kTier1Warps * 32, occ.smem1, stream>>>(
+          reqs, trace_offsets, cfgs, cfg_of_trace, results, timeline, recs,
+          ctl, 1, list1, 0, list2, kTier1Warps * 32);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "replay tier-1 launch");
   pmb::replay_gpool_kernel<kRetryWarps>
       <<<L.retry_warps / kRetryWarps, kRetryWarps * 32, 0, stream>>>(
           reqs, trace_offsets, cfgs, cfg_of_trace, results, timeline, recs,
-          ctl, retry_list, gpool, L.nbmax_g);
+          ctl, list2, gpool, L.nbmax_g);
   e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "replay_gpool_kernel launch");
   return PM_SUCCESS;

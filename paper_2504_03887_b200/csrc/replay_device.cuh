@@ -85,9 +85,12 @@ __device__ __forceinline__ void check_uniform(T v, int line) {
 #define PM_UNIFORM(v) ((void)0)
 #endif
 
+// Allocator constants: the per-request ones in registers, the miss-path
+// ones (segment sizing, capacity) read from the caller's config record.
 struct Cfg {
-  long long small_size, small_buffer, min_large, large_buffer, round_large,
-      alignment, max_split, capacity;
+  const pm_cfg_t* cp;
+  u64 amask;
+  long long max_split;
 };
 
 // Free-block entries (bucket storage), shared memory or HBM.
@@ -129,16 +132,16 @@ struct DirReg {
   u64 dk, da;
   int dp, dc;
   int nb;
-  unsigned used;  // physical buckets in use (bit p)
   int nbmax;
   int lane;
+  unsigned* cta_used;  // CTA-shared bitmap of physical buckets in use
+  int cta_words, cta_buckets;
 
   __device__ __forceinline__ void init(int nbmax_, int lane_) {
     dk = da = ~0ull;
     dp = -1;
     dc = 0;
     nb = 0;
-    used = 0;
     nbmax = nbmax_;
     lane = lane_;
   }
@@ -208,12 +211,34 @@ struct DirReg {
     nb -= 1;
     if (d == 0 && lane == 0) dk = da = 0;
   }
+  // claim a free physical bucket of the CTA-shared pool; -1 if exhausted
   __device__ __forceinline__ int alloc_phys() {
-    const int p = __ffs(~used) - 1;
-    used |= 1u << p;
-    return p;
+    int p = -1;
+    if (lane == 0) {
+      for (int w = 0; w < cta_words && p < 0; ++w) {
+        unsigned v = cta_used[w];
+        while (v != 0xffffffffu) {
+          const int b = __ffs(~v) - 1;
+          const unsigned old = atomicOr(&cta_used[w], 1u << b);
+          if (!(old & (1u << b))) {
+            p = w * 32 + b;
+            break;
+          }
+          v = old | (1u << b);
+        }
+      }
+      if (p >= cta_buckets) p = -1;  // padding bits past the pool
+    }
+    return __shfl_sync(kFull, p, 0);
   }
-  __device__ __forceinline__ void free_phys(int p) { used &= ~(1u << p); }
+  __device__ __forceinline__ void free_phys(int p) {
+    if (lane == 0) atomicAnd(&cta_used[p >> 5], ~(1u << (p & 31)));
+  }
+  // hand every bucket of this warp back to the CTA pool
+  __device__ __forceinline__ void release_all() {
+    if (lane < nb) atomicAnd(&cta_used[dp >> 5], ~(1u << (dp & 31)));
+    nb = 0;
+  }
   __device__ __forceinline__ bool full() const { return nb >= nbmax; }
 };
 
@@ -336,9 +361,11 @@ struct DirMem {
     __syncwarp();
   }
   __device__ __forceinline__ int alloc_phys() {
+    if (ptop == 0) return -1;
     ptop -= 1;
     return pstack[ptop];
   }
+  __device__ __forceinline__ void release_all() { nb = 0; }
   __device__ __forceinline__ void free_phys(int p) {
     __syncwarp();
     pstack[ptop] = p;
@@ -457,8 +484,9 @@ __device__ __forceinline__ bool split_bucket(const Pool& P, D& dir, int d,
   // a full directory first merges an adjacent pair; the caller re-finds
   // its bucket and retries (the merge always frees a directory slot)
   if (dir.full()) return try_merge(P, dir, rec, st, hcmp, lane);
-  const int p = dir.phys(d);
   const int q = dir.alloc_phys();
+  if (q < 0) return try_merge(P, dir, rec, st, hcmp, lane);
+  const int p = dir.phys(d);
   const int base = p * kBucket;
   const u64 k = P.key[base + lane];
   const u64 a = P.addr[base + lane];
@@ -504,6 +532,7 @@ __device__ __forceinline__ int pool_insert(const Pool& P, D& dir, Ctx& c,
                                            int hcmp, int lane) {
   if (dir.nb == 0) {
     const int q = dir.alloc_phys();
+    if (q < 0) return -1;
     dir.insert(0, 0ull, 0ull, q, 0);
   }
   int d = dir.find(k, a);
@@ -609,9 +638,11 @@ __device__ __forceinline__ int best_fit(const Pool& P, const D& dir, u64 lo,
 // allocator.py:86-92
 __device__ __forceinline__ long long segment_size_for(long long rounded,
                                                       const Cfg& c) {
-  if (rounded <= c.small_size) return c.small_buffer;
-  if (rounded <= c.min_large) return c.large_buffer;
-  return ((rounded + c.round_large - 1) / c.round_large) * c.round_large;
+  const pm_cfg_t* cp = c.cp;
+  if (rounded <= cp->k_small_size) return cp->k_small_buffer;
+  if (rounded <= cp->k_min_large_alloc) return cp->k_large_buffer;
+  const long long rl = cp->k_round_large;
+  return ((rounded + rl - 1) / rl) * rl;
 }
 
 // Wholly-free segment (free entry with no allocated neighbour) of largest
@@ -660,8 +691,9 @@ __device__ __forceinline__ void make_room(const Pool& P, D& dir, Ctx& c,
                                           long long seg, const Cfg& cf,
                                           const Recs& rec, const Stage& st,
                                           int hcmp, int lane) {
+  const long long capacity = cf.cp->device_capacity;
   if (cf.max_split >= 0) {
-    while (c.reserved + seg > cf.capacity) {
+    while (c.reserved + seg > capacity) {
       const int id = find_release_candidate(P, dir, cf.max_split, lane);
       if (id < 0) break;
       const long long sz = (long long)(P.key[id] & kSizeMask);
@@ -670,7 +702,7 @@ __device__ __forceinline__ void make_room(const Pool& P, D& dir, Ctx& c,
       c.nseg -= 1;
     }
   }
-  if (c.reserved + seg > cf.capacity) {
+  if (c.reserved + seg > capacity) {
     for (;;) {
       const int id = find_release_candidate(P, dir, -1, lane);
       if (id < 0) break;
@@ -695,15 +727,10 @@ __device__ __forceinline__ void replay_trace(
   const long long n = offs[tr + 1] - e0;
   const pm_cfg_t* cp = cfgs + (cfg_of ? cfg_of[tr] : 0);
   Cfg cf;
-  cf.small_size = cp->k_small_size;
-  cf.small_buffer = cp->k_small_buffer;
-  cf.min_large = cp->k_min_large_alloc;
-  cf.large_buffer = cp->k_large_buffer;
-  cf.round_large = cp->k_round_large;
-  cf.alignment = cp->alignment;
+  cf.cp = cp;
+  cf.amask = (u64)cp->alignment - 1;
   cf.max_split = cp->max_split_size;
-  cf.capacity = cp->device_capacity;
-  const u64 amask = (u64)cf.alignment - 1;
+  const u64 amask = cf.amask;
 
   Recs rec;
   rec.base = rec_base + 4 * (size_t)e0;
@@ -818,9 +845,10 @@ __device__ __forceinline__ void replay_trace(
           } else {
             // miss: new segment (allocator.py:278-288, 244-250)
             const long long seg = segment_size_for((long long)rounded, cf);
-            if (cf.capacity >= 0 && c.reserved + seg > cf.capacity) {
+            const long long capacity = cp->device_capacity;
+            if (capacity >= 0 && c.reserved + seg > capacity) {
               make_room(P, dir, c, seg, cf, rec, st, hcmp, lane);
-              if (c.reserved + seg > cf.capacity) sts = PM_OOM;
+              if (c.reserved + seg > capacity) sts = PM_OOM;
             }
             if (sts == PM_OK && (u64)seg > kSizeMask) sts = PM_SIZE_LIMIT;
             if (sts == PM_OK) {
@@ -980,6 +1008,7 @@ __device__ __forceinline__ void replay_trace(
     if (status != PM_OK) break;
   }
 
+  dir.release_all();
   if (lane == 0) {
     pm_result_t res;
     res.peak_reserved = c.peak_reserved;
@@ -1000,30 +1029,35 @@ __device__ __forceinline__ void replay_trace(
 // ---- kernels -------------------------------------------------------------------
 
 struct Ctl {
-  unsigned work;        // main-kernel work counter
-  unsigned n_retry;     // traces whose free blocks outgrew shared memory
-  unsigned retry_work;  // retry-kernel work counter
-  unsigned pad[61];
+  unsigned work[3];   // work counters: main pass, tier-1 retry, tier-2 retry
+  unsigned n_list[3]; // traces queued for tier 1 / tier 2 (index 1, 2)
+  unsigned pad[58];
 };
 
-// Per-warp region: pool entries (3 x nbmax*32 u64), staging (32 x 24 B),
-// and for the memory directory 2 x nbmax u64 + 3 x nbmax int.
-__host__ __device__ __forceinline__ size_t smem_warp_bytes(int nbmax) {
-  return (size_t)nbmax * kBucket * 24 + 32 * 24;
+// Shared-memory layout of the main kernel (per CTA): the bucket pool
+// (3 x B*32 u64: key, addr, links), WARPS staging areas (32 x 24 B each) and
+// the pool's in-use bitmap.  The HBM retry kernel gives each warp a private
+// region: pool + staging + a memory directory (2 x nbmax u64 + 3 x nbmax int).
+__host__ __device__ __forceinline__ size_t smem_cta_bytes(int buckets,
+                                                          int warps) {
+  return (size_t)buckets * kBucket * 24 + (size_t)warps * 32 * 24 +
+         (size_t)((buckets + 31) / 32) * 4;
 }
 __host__ __device__ __forceinline__ size_t gmem_warp_bytes(int nbmax) {
   return ((size_t)nbmax * kBucket * 24 + 32 * 24 + (size_t)nbmax * 28 + 255) /
          256 * 256;
 }
 
-__device__ __forceinline__ void carve_pool(char* base, int nbmax, Pool& P,
-                                           Stage& st) {
-  const size_t E = (size_t)nbmax * kBucket;
+__device__ __forceinline__ void carve_pool(char* base, int nbuckets, Pool& P) {
+  const size_t E = (size_t)nbuckets * kBucket;
   u64* q = reinterpret_cast<u64*>(base);
   P.key = q;
   P.addr = q + E;
   P.links = q + 2 * E;
-  u64* s = q + 3 * E;
+}
+
+__device__ __forceinline__ void carve_stage(char* base, Stage& st) {
+  u64* s = reinterpret_cast<u64*>(base);
   st.a = s;
   st.k = s + 32;
   st.L = reinterpret_cast<u32*>(s + 64);
@@ -1031,42 +1065,56 @@ __device__ __forceinline__ void carve_pool(char* base, int nbmax, Pool& P,
 }
 
 // Main kernel: persistent warps pull traces (longest first) from a global
-// counter; free blocks in dynamic shared memory, directory in registers.
+// counter.  The CTA's warps share one shared-memory bucket pool (free-block
+// counts vary 10x between traces, so pooling fits far more warps per SM than
+// private worst-case pools); each warp's directory lives in its registers.
 template <int WARPS>
 __global__ void __launch_bounds__(WARPS * 32, 1)
     replay_smem_kernel(const pm_req_t* __restrict__ reqs,
-                       const int64_t* __restrict__ offs, int n_traces,
+                       const int64_t* __restrict__ offs,
                        const pm_cfg_t* __restrict__ cfgs,
                        const int32_t* __restrict__ cfg_of,
-                       const int32_t* __restrict__ order,
                        pm_result_t* __restrict__ results,
                        int64_t* __restrict__ timeline, u64* recs, Ctl* ctl,
-                       int32_t* __restrict__ retry_list, int nbmax) {
+                       int pass, const int32_t* __restrict__ list, int n_host,
+                       int32_t* __restrict__ overflow_list, int buckets) {
   extern __shared__ __align__(16) char smem[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
   Pool P;
+  carve_pool(smem, buckets, P);
   Stage st;
-  carve_pool(smem + (size_t)wib * smem_warp_bytes(nbmax), nbmax, P, st);
+  carve_stage(smem + (size_t)buckets * kBucket * 24 + (size_t)wib * 32 * 24,
+              st);
+  unsigned* used = reinterpret_cast<unsigned*>(
+      smem + (size_t)buckets * kBucket * 24 + (size_t)WARPS * 32 * 24);
+  const int words = (buckets + 31) / 32;
+  for (int i = threadIdx.x; i < words; i += blockDim.x) used[i] = 0u;
+  __syncthreads();
   DirReg dir;
+  dir.cta_used = used;
+  dir.cta_words = words;
+  dir.cta_buckets = buckets;
+  const unsigned n = pass == 0 ? (unsigned)n_host : ctl->n_list[pass];
   for (;;) {
     unsigned t = 0;
-    if (lane == 0) t = atomicAdd(&ctl->work, 1u);
+    if (lane == 0) t = atomicAdd(&ctl->work[pass], 1u);
     t = __shfl_sync(kFull, t, 0);
-    if (t >= (unsigned)n_traces) break;
-    const int tr = order ? order[t] : (int)t;
+    if (t >= n) break;
+    const int tr = list ? list[t] : (int)t;
     replay_trace(tr, reqs, offs, cfgs, cfg_of, results, timeline, recs, P,
-                 dir, nbmax, st, lane);
+                 dir, kBucket, st, lane);
     __syncwarp();
     if (lane == 0 && results[tr].status == PM_POOL_OVERFLOW) {
-      const unsigned k = atomicAdd(&ctl->n_retry, 1u);
-      retry_list[k] = tr;
+      const unsigned k = atomicAdd(&ctl->n_list[pass + 1], 1u);
+      overflow_list[k] = tr;
     }
   }
 }
 
-// Traces whose free blocks outgrew shared memory: the same replay with the
-// entries and the directory in a per-warp HBM region sized for the longest
+// Tier 2 -- traces whose free blocks outgrew even a dedicated 32-bucket
+// shared-memory pool: the same replay with the entries and the directory in
+// a per-warp HBM region sized for the longest
 // trace (free blocks never exceed live allocations + live segments <= 2 x
 // requests, and with every adjacent bucket pair holding > 32 entries a
 // directory of n/8+4 buckets always has room).
@@ -1087,10 +1135,12 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
   char* base = gpool + (size_t)gw * gmem_warp_bytes(nbmax_g);
   Pool P;
   Stage st;
-  carve_pool(base, nbmax_g, P, st);
+  carve_pool(base, nbmax_g, P);
+  carve_stage(base + (size_t)nbmax_g * kBucket * 24, st);
   DirMem dir;
   {
-    u64* q = reinterpret_cast<u64*>(base + smem_warp_bytes(nbmax_g));
+    u64* q = reinterpret_cast<u64*>(base + (size_t)nbmax_g * kBucket * 24 +
+                                    32 * 24);
     dir.dkey = q;
     dir.daddr = q + nbmax_g;
     int* ip = reinterpret_cast<int*>(q + 2 * (size_t)nbmax_g);
@@ -1098,10 +1148,10 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
     dir.cnt = ip + nbmax_g;
     dir.pstack = ip + 2 * nbmax_g;
   }
-  const unsigned n_retry = ctl->n_retry;
+  const unsigned n_retry = ctl->n_list[2];
   for (;;) {
     unsigned t = 0;
-    if (lane == 0) t = atomicAdd(&ctl->retry_work, 1u);
+    if (lane == 0) t = atomicAdd(&ctl->work[2], 1u);
     t = __shfl_sync(kFull, t, 0);
     if (t >= n_retry) break;
     const int tr = retry_list[t];
