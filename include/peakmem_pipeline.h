@@ -1,0 +1,83 @@
+/*
+ * peakmem_pipeline.h -- C ABI of the GPU analysis / link / orchestration
+ * stages of the xMem (arXiv 2504.03887) estimator (csrc/pipeline.cu).
+ *
+ * Host arrays in, host arrays out; device memory is stream-ordered scratch.
+ * Return 0 or a pm_err_t code (include/peakmem_b200.h); the message is in
+ * pm_pipeline_last_error().  Timestamps are integer microseconds; INT64_MIN
+ * stands for Python's None (a never-freed block).
+ *
+ * Reference interface each entry point replaces (paths relative to
+ * /root/reference/pkg/src/peakmem):
+ *   pm_sort_events -> trace.parse_trace's sort + normalize (trace.py:222-236)
+ *   pm_link        -> analysis.build_operator_roots (analysis.py:185-211),
+ *                     analysis.group_memory_events (analysis.py:252-294) and
+ *                     linking.link (linking.py:126-132) + the backward-
+ *                     retained test of orchestration.tag_gradient_blocks
+ *                     (orchestration.py:122-132, linking.py:40-43), as
+ *                     called by orchestration.analyze (orchestration.py:107)
+ *   pm_link_roots  -> linking.link on caller-given roots and blocks
+ *   pm_orchestrate -> orchestration.build_sequence's per-block rewrites,
+ *                     emission and total order (orchestration.py:270-387)
+ */
+#ifndef PEAKMEM_PIPELINE_H
+#define PEAKMEM_PIPELINE_H
+
+#include <stdint.h>
+
+#include "peakmem_b200.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+const char* pm_pipeline_last_error(void);
+
+int pm_sort_events(const double* ts, const double* dur, int64_t n,
+                   int64_t* perm, int64_t* start, int64_t* duration,
+                   void* stream);
+
+int pm_link(int64_t n_ops, const int64_t* op_start, const int64_t* op_end,
+            const int64_t* op_seq, int64_t n_inst, const int64_t* in_start,
+            const int64_t* in_addr, const int64_t* in_nbytes,
+            int64_t n_leaves, const int64_t* l_start, const int64_t* l_end,
+            int64_t* op_root, int64_t* n_roots_out, int64_t* root_op,
+            int64_t* root_start, int64_t* root_end, int64_t* root_seq_off,
+            int64_t* root_seq, int64_t* root_leaf, int64_t* bwd_off,
+            int64_t* bwd_root, int64_t bwd_cap, int64_t* n_bwd_out,
+            int64_t* n_blocks_out, int64_t* b_inst, int64_t* b_alloc,
+            int64_t* b_size, int64_t* b_free, int32_t* b_role,
+            int64_t* b_prof, int64_t* b_root, void* stream);
+
+int pm_link_roots(int64_t n_roots, const int64_t* root_start,
+                  const int64_t* root_end, const int64_t* root_seq_off,
+                  const int64_t* root_seq, int64_t n_leaves,
+                  const int64_t* l_start, const int64_t* l_end,
+                  int64_t n_blocks, const int64_t* b_alloc,
+                  const int64_t* b_free, int64_t* root_leaf, int64_t* bwd_off,
+                  int64_t* bwd_root, int64_t bwd_cap, int64_t* n_bwd_out,
+                  int32_t* b_role, int64_t* b_prof, int64_t* b_root,
+                  void* stream);
+
+int pm_orchestrate(int64_t nb, const int64_t* b_alloc, const int64_t* b_size,
+                   const int64_t* b_free, const int32_t* b_role,
+                   int32_t n_spans, const int64_t* span_start,
+                   const int64_t* span_end, const int64_t* span_iter,
+                   int32_t n_param, const int64_t* param_sizes,
+                   int32_t n_windows, const int64_t* win_start,
+                   const int64_t* win_end, int32_t n_zg, const int64_t* zg,
+                   int32_t clones, int64_t tpl_start, int64_t tpl_end,
+                   int64_t shift, int64_t n_batch, const int64_t* batch_vts,
+                   const int64_t* batch_size, const int32_t* batch_kind,
+                   const int64_t* batch_it, const int64_t* batch_j,
+                   int64_t req_cap, int64_t* n_req_out, int64_t* n_model_out,
+                   int64_t* o_raw, int32_t* o_kind, int64_t* o_size,
+                   int64_t* o_vts, int32_t* o_tag, int64_t* o_a, int64_t* o_b,
+                   int32_t* o_role, pm_req_t* o_packed, int32_t* fb_role,
+                   int64_t* fb_free, int32_t* fb_flags, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PEAKMEM_PIPELINE_H */

@@ -36,4 +36,36 @@ from .errors import (
     ZeroSize,
 )
 
+from .analysis import (
+    AnnotationMarker,
+    BlockRole,
+    LayerNode,
+    MarkerKind,
+    MemoryBlock,
+    OperatorNode,
+    build_layer_tree,
+    build_operator_roots,
+    extract_markers,
+    group_memory_events,
+)
+from .estimator import EstimateReport, PeakMemoryEstimator
+from .linking import LayerMemoryProfile, link
+from .metrics import predict_oom
+from .orchestration import (
+    AnalyzedTrace,
+    MemoryRequest,
+    RequestKind,
+    RequestSequence,
+    analyze,
+    build_sequence,
+)
+from .trace import (
+    EventCategory,
+    SidecarConfig,
+    TraceBundle,
+    TraceEvent,
+    load_sidecar,
+    parse_trace,
+)
+
 __version__ = "0.1.0"

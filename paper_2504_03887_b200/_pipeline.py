@@ -1,0 +1,232 @@
+"""ctypes binding of the analysis / link / orchestration kernels
+(csrc/pipeline.cu, built into lib/libpeakmem_pipeline.so).  No CPU fallback:
+a missing library or device raises EngineUnavailable."""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _native
+from ._native import LIB_DIR, REQ_DTYPE
+from .errors import EngineUnavailable
+
+LIB_PATH = LIB_DIR / "libpeakmem_pipeline.so"
+EXPORTED_SYMBOLS = ("pm_pipeline_last_error", "pm_sort_events", "pm_link",
+                    "pm_link_roots", "pm_orchestrate")
+NONE = np.iinfo(np.int64).min
+
+_lib = None
+
+
+def load():
+    global _lib
+    if _lib is None:
+        if not LIB_PATH.exists():
+            raise EngineUnavailable(
+                f"{LIB_PATH} is not built; run __graft_entry__.build()")
+        lib = ctypes.CDLL(str(LIB_PATH))
+        lib.pm_pipeline_last_error.restype = ctypes.c_char_p
+        lib.pm_pipeline_last_error.argtypes = []
+        for name in EXPORTED_SYMBOLS[1:]:
+            getattr(lib, name).restype = ctypes.c_int
+        _lib = lib
+    return _lib
+
+
+def _p(a):
+    return ctypes.c_void_p(None if a is None else a.ctypes.data)
+
+
+def _i64(a):
+    return np.ascontiguousarray(a, dtype=np.int64)
+
+
+def _check(rc: int, lib) -> None:
+    if rc != 0:
+        msg = lib.pm_pipeline_last_error().decode(errors="replace")
+        raise RuntimeError(f"peakmem_b200 pipeline error {rc}: {msg}")
+
+
+def _stream():
+    try:
+        import torch
+        return torch.cuda.current_stream().cuda_stream
+    except Exception:  # pragma: no cover
+        return 0
+
+
+def sort_events(ts: np.ndarray, dur: np.ndarray):
+    """Stable device sort by raw ts + fp64 normalization (trace.py:222-236).
+    Returns (perm, start, duration) in event-id order."""
+    lib = load()
+    _native.require_device()
+    n = len(ts)
+    ts = np.ascontiguousarray(ts, dtype=np.float64)
+    dur = np.ascontiguousarray(dur, dtype=np.float64)
+    perm = np.empty(n, np.int64)
+    start = np.empty(n, np.int64)
+    duration = np.empty(n, np.int64)
+    _check(lib.pm_sort_events(_p(ts), _p(dur), ctypes.c_int64(n), _p(perm),
+                              _p(start), _p(duration),
+                              ctypes.c_void_p(_stream())), lib)
+    return perm, start, duration
+
+
+class LinkResult:
+    """Columnar output of pm_link (see csrc/pipeline.cu)."""
+
+
+def link(op_start, op_end, op_seq, in_start, in_addr, in_nbytes,
+         l_start, l_end) -> LinkResult:
+    lib = load()
+    _native.require_device()
+    op_start, op_end, op_seq = map(_i64, (op_start, op_end, op_seq))
+    in_start, in_addr, in_nbytes = map(_i64, (in_start, in_addr, in_nbytes))
+    l_start, l_end = map(_i64, (l_start, l_end))
+    no, ni, nl = len(op_start), len(in_start), len(l_start)
+    r = LinkResult()
+    r.op_root = np.empty(no, np.int64)
+    root_op = np.empty(max(no, 1), np.int64)
+    root_start = np.empty(max(no, 1), np.int64)
+    root_end = np.empty(max(no, 1), np.int64)
+    root_seq_off = np.empty(no + 1, np.int64)
+    root_seq = np.empty(max(no, 1), np.int64)
+    root_leaf = np.empty(max(no, 1), np.int64)
+    bwd_off = np.empty(nl + 1, np.int64)
+    b_inst = np.empty(max(ni, 1), np.int64)
+    b_alloc = np.empty(max(ni, 1), np.int64)
+    b_size = np.empty(max(ni, 1), np.int64)
+    b_free = np.empty(max(ni, 1), np.int64)
+    b_role = np.empty(max(ni, 1), np.int32)
+    b_prof = np.empty(max(ni, 1), np.int64)
+    b_root = np.empty(max(ni, 1), np.int64)
+    n_roots = ctypes.c_int64(0)
+    n_bwd = ctypes.c_int64(0)
+    n_blocks = ctypes.c_int64(0)
+    cap = max(4 * no, 16)
+    while True:
+        bwd_root = np.empty(cap, np.int64)
+        rc = lib.pm_link(
+            ctypes.c_int64(no), _p(op_start), _p(op_end), _p(op_seq),
+            ctypes.c_int64(ni), _p(in_start), _p(in_addr), _p(in_nbytes),
+            ctypes.c_int64(nl), _p(l_start), _p(l_end), _p(r.op_root),
+            ctypes.byref(n_roots), _p(root_op), _p(root_start), _p(root_end),
+            _p(root_seq_off), _p(root_seq), _p(root_leaf), _p(bwd_off),
+            _p(bwd_root), ctypes.c_int64(cap), ctypes.byref(n_bwd),
+            ctypes.byref(n_blocks), _p(b_inst), _p(b_alloc), _p(b_size),
+            _p(b_free), _p(b_role), _p(b_prof), _p(b_root),
+            ctypes.c_void_p(_stream()))
+        if rc == 3 and n_bwd.value > cap:  # PM_ERR_WORKSPACE_TOO_SMALL
+            cap = n_bwd.value
+            continue
+        _check(rc, lib)
+        break
+    nr, nb = n_roots.value, n_blocks.value
+    r.n_roots, r.n_blocks = nr, nb
+    r.root_op, r.root_start, r.root_end = root_op[:nr], root_start[:nr], root_end[:nr]
+    r.root_seq_off = root_seq_off[:nr + 1]
+    r.root_seq = root_seq[:int(r.root_seq_off[-1]) if nr else 0]
+    r.root_leaf = root_leaf[:nr]
+    r.bwd_off = bwd_off
+    r.bwd_root = bwd_root[:n_bwd.value]
+    r.b_inst, r.b_alloc, r.b_size = b_inst[:nb], b_alloc[:nb], b_size[:nb]
+    r.b_free, r.b_role, r.b_prof, r.b_root = (b_free[:nb], b_role[:nb],
+                                              b_prof[:nb], b_root[:nb])
+    return r
+
+
+def link_roots(root_start, root_end, root_seq_off, root_seq, l_start, l_end,
+               b_alloc, b_free) -> LinkResult:
+    """The join on GIVEN roots (linking.py:126-132 with any root set)."""
+    lib = load()
+    _native.require_device()
+    root_start, root_end, root_seq_off, root_seq = map(
+        _i64, (root_start, root_end, root_seq_off, root_seq))
+    l_start, l_end, b_alloc, b_free = map(_i64, (l_start, l_end, b_alloc, b_free))
+    nr, nl, nb = len(root_start), len(l_start), len(b_alloc)
+    r = LinkResult()
+    r.root_leaf = np.empty(max(nr, 1), np.int64)
+    r.bwd_off = np.empty(nl + 1, np.int64)
+    r.b_role = np.empty(max(nb, 1), np.int32)
+    r.b_prof = np.empty(max(nb, 1), np.int64)
+    r.b_root = np.empty(max(nb, 1), np.int64)
+    n_bwd = ctypes.c_int64(0)
+    cap = max(4 * nr, 16)
+    while True:
+        bwd_root = np.empty(cap, np.int64)
+        rc = lib.pm_link_roots(
+            ctypes.c_int64(nr), _p(root_start), _p(root_end), _p(root_seq_off),
+            _p(root_seq), ctypes.c_int64(nl), _p(l_start), _p(l_end),
+            ctypes.c_int64(nb), _p(b_alloc), _p(b_free), _p(r.root_leaf),
+            _p(r.bwd_off), _p(bwd_root), ctypes.c_int64(cap),
+            ctypes.byref(n_bwd), _p(r.b_role), _p(r.b_prof), _p(r.b_root),
+            ctypes.c_void_p(_stream()))
+        if rc == 3 and n_bwd.value > cap:
+            cap = n_bwd.value
+            continue
+        _check(rc, lib)
+        break
+    r.root_leaf = r.root_leaf[:nr]
+    r.bwd_root = bwd_root[:n_bwd.value]
+    r.b_role, r.b_prof, r.b_root = r.b_role[:nb], r.b_prof[:nb], r.b_root[:nb]
+    return r
+
+
+class OrchResult:
+    """Ordered request sequence from pm_orchestrate."""
+
+
+def orchestrate(b_alloc, b_size, b_free, b_role, spans, param_sizes, windows,
+                zg, clones, tpl, shift, batch) -> OrchResult:
+    """spans: (start, end, iteration) arrays; windows: (start, end) arrays;
+    tpl: (start, end); batch: (vts, size, kind, iteration, j) arrays."""
+    lib = load()
+    _native.require_device()
+    b_alloc, b_size, b_free = map(_i64, (b_alloc, b_size, b_free))
+    b_role = np.ascontiguousarray(b_role, dtype=np.int32)
+    sp_s, sp_e, sp_i = map(_i64, spans)
+    param_sizes = _i64(param_sizes)
+    w_s, w_e = map(_i64, windows)
+    zg = _i64(zg)
+    bv, bs, bk, bi, bj = batch
+    bv, bs, bi, bj = map(_i64, (bv, bs, bi, bj))
+    bk = np.ascontiguousarray(bk, dtype=np.int32)
+    nb = len(b_alloc)
+    cap = len(param_sizes) * 0 + nb + len(bv) + 2 * nb * (1 + max(clones, 0)) + 16
+    o = OrchResult()
+    o.raw = np.empty(cap, np.int64)
+    o.kind = np.empty(cap, np.int32)
+    o.size = np.empty(cap, np.int64)
+    o.vts = np.empty(cap, np.int64)
+    o.tag = np.empty(cap, np.int32)
+    o.a = np.empty(cap, np.int64)
+    o.b = np.empty(cap, np.int64)
+    o.role = np.empty(cap, np.int32)
+    o.packed = np.empty(cap, REQ_DTYPE)
+    o.fb_role = np.empty(max(nb, 1), np.int32)
+    o.fb_free = np.empty(max(nb, 1), np.int64)
+    o.fb_flags = np.empty(max(nb, 1), np.int32)
+    n_req = ctypes.c_int64(0)
+    n_model = ctypes.c_int64(0)
+    _check(lib.pm_orchestrate(
+        ctypes.c_int64(nb), _p(b_alloc), _p(b_size), _p(b_free), _p(b_role),
+        ctypes.c_int32(len(sp_s)), _p(sp_s), _p(sp_e), _p(sp_i),
+        ctypes.c_int32(len(param_sizes)), _p(param_sizes),
+        ctypes.c_int32(len(w_s)), _p(w_s), _p(w_e), ctypes.c_int32(len(zg)),
+        _p(zg), ctypes.c_int32(clones), ctypes.c_int64(tpl[0]),
+        ctypes.c_int64(tpl[1]), ctypes.c_int64(shift),
+        ctypes.c_int64(len(bv)), _p(bv), _p(bs), _p(bk), _p(bi), _p(bj),
+        ctypes.c_int64(cap), ctypes.byref(n_req), ctypes.byref(n_model),
+        _p(o.raw), _p(o.kind), _p(o.size), _p(o.vts), _p(o.tag), _p(o.a),
+        _p(o.b), _p(o.role), _p(o.packed), _p(o.fb_role), _p(o.fb_free),
+        _p(o.fb_flags), ctypes.c_void_p(_stream())), lib)
+    o.n_model = n_model.value
+    n = n_req.value
+    o.n = n
+    if n >= 0:
+        for f in ("raw", "kind", "size", "vts", "tag", "a", "b", "role", "packed"):
+            setattr(o, f, getattr(o, f)[:n])
+    o.fb_role, o.fb_free, o.fb_flags = o.fb_role[:nb], o.fb_free[:nb], o.fb_flags[:nb]
+    return o

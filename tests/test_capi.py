@@ -18,10 +18,11 @@ from paper_2504_03887_b200.errors import ZeroSize
 
 MIB = 1 << 20
 HEADER = REPO / "include" / "peakmem_b200.h"
+PIPE_HEADER = REPO / "include" / "peakmem_pipeline.h"
 
 
-def header_functions():
-    text = HEADER.read_text()
+def header_functions(header=HEADER):
+    text = header.read_text()
     return sorted(set(re.findall(r"^\s*(?:int|const char\*)\s+(pm_\w+)\(",
                                  text, re.M)))
 
@@ -41,7 +42,22 @@ def test_library_exports_every_declared_symbol():
     for sym in header_functions():
         assert sym in exported, sym
     loaded = _native.load_library()
-    assert loaded.pm_version() == 1
+    assert loaded.pm_version() == 2
+
+
+def test_pipeline_library_exports_every_declared_symbol():
+    from paper_2504_03887_b200 import _pipeline
+    assert header_functions(PIPE_HEADER) == sorted(_pipeline.EXPORTED_SYMBOLS)
+    lib = _pipeline.LIB_PATH
+    if not lib.exists():
+        import __graft_entry__
+        __graft_entry__.build()
+    out = subprocess.run(["nm", "-D", "--defined-only", str(lib)],
+                         capture_output=True, text=True, check=True).stdout
+    exported = set(re.findall(r"\bT (pm_\w+)", out))
+    for sym in header_functions(PIPE_HEADER):
+        assert sym in exported, sym
+    _pipeline.load()
 
 
 def test_library_is_sm100a():

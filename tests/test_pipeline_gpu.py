@@ -1,0 +1,71 @@
+"""GPU parity of the analysis -> link -> orchestration -> estimate path.
+
+Every case is compared with golden vectors produced by the reference itself
+(tests/golden/make_golden_pipeline.py): normalized events, layer tree with
+per-layer forward / backward ops and retained / temporary blocks (the
+event -> operator -> layer linkage), operator roots, markers, blocks with
+roles, request sequences for 1-3 iterations (incl. cloning), the blocks'
+roles / lifetimes after orchestration, and the byte-exact estimate reports
+(three allocator configurations).
+"""
+
+from __future__ import annotations
+
+import gzip
+import json
+import logging
+from pathlib import Path
+
+import pytest
+
+import paper_2504_03887_b200 as api
+from conftest import GOLDEN, golden
+from pipeline_cases import CASES, case_records, views
+
+pytestmark = [pytest.mark.gpu, pytest.mark.usefixtures("require_gpu")]
+logging.disable(logging.WARNING)
+
+FIXTURES = ["tiny_mlp_sgd", "tiny_mlp_adam", "tiny_mlp_sgd_pregrad"]
+
+
+def fixture_bundle(name, tmp_path):
+    trace = tmp_path / f"{name}.json"
+    with gzip.open(GOLDEN / "traces" / f"{name}.trace.json.gz", "rb") as f:
+        trace.write_bytes(f.read())
+    side = api.load_sidecar(GOLDEN / "traces" / f"{name}.sidecar.json")
+    return api.parse_trace(trace, sidecar=side)
+
+
+def case_bundle(case, tmp_path):
+    recs, side = case_records(case)
+    p = tmp_path / f"{case['name']}.json"
+    p.write_text(json.dumps({"traceEvents": recs}))
+    sc = api.SidecarConfig(param_sizes=tuple(side["param_sizes"]),
+                           batch_bytes=tuple(side["batch_bytes"]),
+                           optimizer_name=side["optimizer"],
+                           device_capacity=side.get("device_capacity_bytes", 0),
+                           initial_memory=side.get("initial_memory_bytes", 0))
+    return api.parse_trace(p, sidecar=sc)
+
+
+def compare(got: dict, want: dict):
+    for key in want:
+        if key == "golden_report":
+            continue
+        assert got[key] == want[key], key
+
+
+@pytest.mark.parametrize("name", FIXTURES)
+def test_fixture_pipeline_matches_reference(name, tmp_path):
+    bundle = fixture_bundle(name, tmp_path)
+    want = golden("pipeline_golden.json")[name]
+    compare(views(api, bundle), want)
+    # the committed golden report, byte for byte (test_acceptance.py:347-359)
+    assert api.PeakMemoryEstimator().estimate(bundle).canonical_json() == \
+        want["golden_report"]
+
+
+@pytest.mark.parametrize("case", CASES, ids=[c["name"] for c in CASES])
+def test_generated_pipeline_matches_reference(case, tmp_path):
+    bundle = case_bundle(case, tmp_path)
+    compare(views(api, bundle), golden("pipeline_golden.json")[case["name"]])
