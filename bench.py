@@ -58,18 +58,6 @@ def parse_args():
     return ap.parse_args()
 
 
-def shard(lengths: np.ndarray, n: int) -> list[np.ndarray]:
-    """Greedy LPT: longest trace to the least-loaded rank."""
-    order = np.argsort(-lengths, kind="stable")
-    loads = np.zeros(n, dtype=np.int64)
-    parts: list[list[int]] = [[] for _ in range(n)]
-    for t in order:
-        r = int(np.argmin(loads))
-        parts[r].append(int(t))
-        loads[r] += lengths[t]
-    return [np.array(sorted(p), dtype=np.int64) for p in parts]
-
-
 def read_peak():
     p = REPO / "MEASURED_PEAKS.json"
     try:
@@ -191,7 +179,8 @@ def main():
     counts = np.zeros(args.traces, dtype=np.int64)
     lib.pm_synth_counts(0, args.traces, counts.ctypes.data,
                         len(os.sched_getaffinity(0)))
-    mine = shard(counts, world)[rank]
+    from paper_2504_03887_b200.shard import lpt_shards
+    mine = lpt_shards(counts, world)[rank]
     # generate the shard's traces contiguously into pinned host memory
     offs = np.zeros(len(mine) + 1, dtype=np.int64)
     np.cumsum(counts[mine], out=offs[1:])

@@ -134,6 +134,8 @@ def views(api, bundle) -> dict:
         after = [[b.block_id, b.free_time, b.role.value] for b in a2.blocks]
         out[f"seq{it}"] = {
             "n": len(seq.requests),
+            "req_sha256": digest([[r.kind.value, r.block_id, r.size, r.virtual_ts]
+                                  for r in seq.requests]),
             "sha256": digest(seq.to_json_dict()),
             "boundaries": seq.iteration_boundaries,
             "blocks_after_sha256": digest(after),

@@ -69,3 +69,22 @@ def test_fixture_pipeline_matches_reference(name, tmp_path):
 def test_generated_pipeline_matches_reference(case, tmp_path):
     bundle = case_bundle(case, tmp_path)
     compare(views(api, bundle), golden("pipeline_golden.json")[case["name"]])
+
+
+@pytest.mark.parametrize("seed,kw", [
+    (101, {"layers": 160, "leaves": 4, "iterations": 3}),
+    (102, {"layers": 80, "leaves": 6, "iterations": 1, "optimizer": "sgd"}),
+    (103, {"layers": 120, "leaves": 3, "iterations": 4, "zero_grad": "pre-backward"}),
+])
+def test_large_generated_pipeline_vs_oracle(seed, kw, tmp_path):
+    """Traces too large for committed goldens: GPU vs the pinned oracle."""
+    from oracle import pipeline as op
+    case = {"name": f"large_{seed}", "seed": seed, "kw": kw}
+    records, side = case_records(case)
+    bundle = case_bundle(case, tmp_path)
+    events = op.normalize(records)
+    for it in (1, 2, 3):
+        want = op.build_sequence(events, side, it)
+        got = api.build_sequence(api.analyze(bundle), iterations=it)
+        assert [(r.kind.value, r.block_id, r.size, r.virtual_ts)
+                for r in got.requests] == want, it
