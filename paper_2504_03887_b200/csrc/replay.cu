@@ -174,12 +174,21 @@ int pm_replay_workspace_bytes(int64_t total_events, int64_t max_trace_events,
   return PM_SUCCESS;
 }
 
-int pm_replay_batch(const pm_req_t* reqs, const int64_t* trace_offsets,
-                    int32_t n_traces, const pm_cfg_t* cfgs,
-                    const int32_t* cfg_of_trace, const int32_t* trace_order,
-                    pm_result_t* results, int64_t* timeline, void* workspace,
-                    size_t workspace_bytes, int64_t total_events,
-                    int64_t max_trace_events, void* stream_) {
+}  // extern "C"
+
+namespace {
+
+// pm_replay_batch with optional streamed input: when `ready` is non-null the
+// main kernel waits, per trace, for the flag of the group (group_end[g] =
+// traces consumed through group g) the copy engine writes after the group.
+int replay_batch_impl(const pm_req_t* reqs, const int64_t* trace_offsets,
+                      int32_t n_traces, const pm_cfg_t* cfgs,
+                      const int32_t* cfg_of_trace, const int32_t* trace_order,
+                      pm_result_t* results, int64_t* timeline, void* workspace,
+                      size_t workspace_bytes, int64_t total_events,
+                      int64_t max_trace_events, void* stream_,
+                      const unsigned* group_end, int n_groups,
+                      const unsigned* ready) {
   if (n_traces < 0 || total_events < 0 || max_trace_events < 0)
     return fail(PM_ERR_INVALID_ARGUMENT, "pm_replay_batch: negative size");
   if (n_traces == 0) return PM_SUCCESS;
@@ -219,7 +228,7 @@ int pm_replay_batch(const pm_req_t* reqs, const int64_t* trace_offsets,
 #define PM_LAUNCH_MAIN(W)                                                     \
   pmb::replay_smem_kernel<W><<<(unsigned)grid, W * 32, occ.smem, stream>>>(  \
       reqs, trace_offsets, cfgs, cfg_of_trace, results, timeline, recs, ctl, \
-      0, trace_order, n_traces, list1, occ.buckets)
+      0, trace_order, n_traces, list1, occ.buckets, group_end, n_groups, ready)
   if (occ.warps == 12)
     PM_LAUNCH_MAIN(12);
   else
@@ -235,7 +244,7 @@ int pm_replay_batch(const pm_req_t* reqs, const int64_t* trace_offsets,
   pmb::replay_smem_kernel<kTier1Warps>
       <<<(unsigned)grid1, kTier1Warps * 32, occ.smem1, stream>>>(
           reqs, trace_offsets, cfgs, cfg_of_trace, results, timeline, recs,
-          ctl, 1, list1, 0, list2, kTier1Warps * 32);
+          ctl, 1, list1, 0, list2, kTier1Warps * 32, nullptr, 0, nullptr);
   e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "replay tier-1 launch");
   pmb::replay_gpool_kernel<kRetryWarps>
@@ -245,6 +254,22 @@ int pm_replay_batch(const pm_req_t* reqs, const int64_t* trace_offsets,
   e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "replay_gpool_kernel launch");
   return PM_SUCCESS;
+}
+
+}  // namespace
+
+extern "C" {
+
+int pm_replay_batch(const pm_req_t* reqs, const int64_t* trace_offsets,
+                    int32_t n_traces, const pm_cfg_t* cfgs,
+                    const int32_t* cfg_of_trace, const int32_t* trace_order,
+                    pm_result_t* results, int64_t* timeline, void* workspace,
+                    size_t workspace_bytes, int64_t total_events,
+                    int64_t max_trace_events, void* stream_) {
+  return replay_batch_impl(reqs, trace_offsets, n_traces, cfgs, cfg_of_trace,
+                           trace_order, results, timeline, workspace,
+                           workspace_bytes, total_events, max_trace_events,
+                           stream_, nullptr, 0, nullptr);
 }
 
 int pm_replay_host(const pm_req_t* reqs, const int64_t* trace_offsets,
@@ -271,13 +296,27 @@ int pm_replay_host(const pm_req_t* reqs, const int64_t* trace_offsets,
     for (int32_t i = 0; i < n_traces; ++i)
       if (cfg_of_trace[i] < 0 || cfg_of_trace[i] >= n_cfgs)
         return fail(PM_ERR_INVALID_ARGUMENT, "pm_replay_host: cfg index out of range");
-  // longest trace first: the persistent warps then finish together
+  // Streamed upload: G contiguous trace groups, each copied (copy stream)
+  // and then flagged with a 4-byte DMA write; the kernel consumes groups in
+  // order, longest trace first within a group, so replay overlaps the H2D.
+  const size_t bytes_in = 16 * (size_t)total;
+  int G = (int)(bytes_in / (256u << 20));
+  if (G < 1) G = 1;
+  if (G > 64) G = 64;
+  if (G > n_traces) G = n_traces;
+  std::vector<int32_t> gfirst(G + 1);
+  for (int g = 0; g <= G; ++g) gfirst[g] = (int32_t)(((int64_t)n_traces * g) / G);
   std::vector<int32_t> order(n_traces);
-  for (int32_t i = 0; i < n_traces; ++i) order[i] = i;
-  std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) {
-    return trace_offsets[a + 1] - trace_offsets[a] >
-           trace_offsets[b + 1] - trace_offsets[b];
-  });
+  std::vector<unsigned> group_end(G);
+  for (int g = 0; g < G; ++g) {
+    for (int32_t i = gfirst[g]; i < gfirst[g + 1]; ++i) order[i] = i;
+    std::stable_sort(order.begin() + gfirst[g], order.begin() + gfirst[g + 1],
+                     [&](int32_t a, int32_t b) {
+                       return trace_offsets[a + 1] - trace_offsets[a] >
+                              trace_offsets[b + 1] - trace_offsets[b];
+                     });
+    group_end[g] = (unsigned)gfirst[g + 1];
+  }
   const Layout L = layout_for(total, max_ev, n_traces);
   cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
   const size_t b_reqs = align_up(16 * (size_t)(total > 0 ? total : 1), 256);
@@ -287,12 +326,36 @@ int pm_replay_host(const pm_req_t* reqs, const int64_t* trace_offsets,
   const size_t b_order = b_cfgof;
   const size_t b_res = align_up(sizeof(pm_result_t) * (size_t)n_traces, 256);
   const size_t b_tl = timeline ? align_up(16 * (size_t)(total > 0 ? total : 1), 256) : 0;
-  const size_t bytes =
-      b_reqs + b_offs + b_cfgs + b_cfgof + b_order + b_res + b_tl + L.total;
+  const size_t b_grp = align_up(8 * (size_t)G, 256);
+  const size_t bytes = b_reqs + b_offs + b_cfgs + b_cfgof + b_order + b_res +
+                       b_tl + 2 * b_grp + L.total;
   keep_pool_mapped();
+  static unsigned* one = nullptr;  // pinned source of the group flags
+  {
+    static std::mutex mu;
+    std::lock_guard<std::mutex> g(mu);
+    if (!one) {
+      cudaError_t e = cudaHostAlloc((void**)&one, sizeof(unsigned), cudaHostAllocPortable);
+      if (e != cudaSuccess) return cuda_fail(e, "cudaHostAlloc");
+      *one = 1u;
+    }
+  }
+  cudaStream_t cs = nullptr;
+  cudaError_t e = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaStreamCreate");
+  cudaEvent_t zeroed = nullptr;
+  e = cudaEventCreateWithFlags(&zeroed, cudaEventDisableTiming);
+  if (e != cudaSuccess) {
+    cudaStreamDestroy(cs);
+    return cuda_fail(e, "cudaEventCreate");
+  }
   void* dmem = nullptr;
-  cudaError_t e = cudaMallocAsync(&dmem, bytes, stream);
-  if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync");
+  e = cudaMallocAsync(&dmem, bytes, stream);
+  if (e != cudaSuccess) {
+    cudaEventDestroy(zeroed);
+    cudaStreamDestroy(cs);
+    return cuda_fail(e, "cudaMallocAsync");
+  }
   char* p = static_cast<char*>(dmem);
   pm_req_t* d_reqs = reinterpret_cast<pm_req_t*>(p);
   p += b_reqs;
@@ -308,6 +371,10 @@ int pm_replay_host(const pm_req_t* reqs, const int64_t* trace_offsets,
   p += b_res;
   int64_t* d_tl = timeline ? reinterpret_cast<int64_t*>(p) : nullptr;
   p += b_tl;
+  unsigned* d_gend = reinterpret_cast<unsigned*>(p);
+  p += b_grp;
+  unsigned* d_ready = reinterpret_cast<unsigned*>(p);
+  p += b_grp;
   void* d_ws = p;
   int rc = PM_SUCCESS;
 #define PM_CHECK(call, what)                 \
@@ -318,9 +385,6 @@ int pm_replay_host(const pm_req_t* reqs, const int64_t* trace_offsets,
       goto done;                             \
     }                                        \
   } while (0)
-  if (total > 0)
-    PM_CHECK(cudaMemcpyAsync(d_reqs, reqs, 16 * (size_t)total,
-                             cudaMemcpyHostToDevice, stream), "H2D requests");
   PM_CHECK(cudaMemcpyAsync(d_offs, trace_offsets, 8 * (size_t)(n_traces + 1),
                            cudaMemcpyHostToDevice, stream), "H2D offsets");
   PM_CHECK(cudaMemcpyAsync(d_cfgs, cfgs, sizeof(pm_cfg_t) * (size_t)n_cfgs,
@@ -330,11 +394,24 @@ int pm_replay_host(const pm_req_t* reqs, const int64_t* trace_offsets,
                              cudaMemcpyHostToDevice, stream), "H2D cfg_of");
   PM_CHECK(cudaMemcpyAsync(d_order, order.data(), 4 * (size_t)n_traces,
                            cudaMemcpyHostToDevice, stream), "H2D order");
+  PM_CHECK(cudaMemcpyAsync(d_gend, group_end.data(), 4 * (size_t)G,
+                           cudaMemcpyHostToDevice, stream), "H2D groups");
+  PM_CHECK(cudaMemsetAsync(d_ready, 0, 4 * (size_t)G, stream), "memset flags");
   if (d_tl)  // entries past an OOM / error stay zero, as on the host side
     PM_CHECK(cudaMemsetAsync(d_tl, 0, b_tl, stream), "memset timeline");
-  rc = pm_replay_batch(d_reqs, d_offs, n_traces, d_cfgs,
-                       cfg_of_trace ? d_cfgof : nullptr, d_order, d_res, d_tl,
-                       d_ws, L.total, total, max_ev, stream_);
+  PM_CHECK(cudaEventRecord(zeroed, stream), "event record");
+  PM_CHECK(cudaStreamWaitEvent(cs, zeroed, 0), "stream wait");
+  for (int g = 0; g < G; ++g) {
+    const int64_t e0 = trace_offsets[gfirst[g]], e1 = trace_offsets[gfirst[g + 1]];
+    if (e1 > e0)
+      PM_CHECK(cudaMemcpyAsync(d_reqs + e0, reqs + e0, 16 * (size_t)(e1 - e0),
+                               cudaMemcpyHostToDevice, cs), "H2D requests");
+    PM_CHECK(cudaMemcpyAsync(d_ready + g, one, sizeof(unsigned),
+                             cudaMemcpyHostToDevice, cs), "H2D flag");
+  }
+  rc = replay_batch_impl(d_reqs, d_offs, n_traces, d_cfgs,
+                         cfg_of_trace ? d_cfgof : nullptr, d_order, d_res, d_tl,
+                         d_ws, L.total, total, max_ev, stream_, d_gend, G, d_ready);
   if (rc != PM_SUCCESS) goto done;
   PM_CHECK(cudaMemcpyAsync(results, d_res, sizeof(pm_result_t) * (size_t)n_traces,
                            cudaMemcpyDeviceToHost, stream), "D2H results");
@@ -343,9 +420,15 @@ int pm_replay_host(const pm_req_t* reqs, const int64_t* trace_offsets,
                              cudaMemcpyDeviceToHost, stream), "D2H timeline");
 done:
 #undef PM_CHECK
+  {
+    cudaError_t e2 = cudaStreamSynchronize(cs);
+    if (rc == PM_SUCCESS && e2 != cudaSuccess) rc = cuda_fail(e2, "copy stream");
+  }
   cudaFreeAsync(dmem, stream);
   e = cudaStreamSynchronize(stream);
   if (rc == PM_SUCCESS && e != cudaSuccess) rc = cuda_fail(e, "cudaStreamSynchronize");
+  cudaEventDestroy(zeroed);
+  cudaStreamDestroy(cs);
   return rc;
 }
 

@@ -1077,7 +1077,9 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
                        pm_result_t* __restrict__ results,
                        int64_t* __restrict__ timeline, u64* recs, Ctl* ctl,
                        int pass, const int32_t* __restrict__ list, int n_host,
-                       int32_t* __restrict__ overflow_list, int buckets) {
+                       int32_t* __restrict__ overflow_list, int buckets,
+                       const unsigned* __restrict__ group_end, int n_groups,
+                       const volatile unsigned* ready) {
   extern __shared__ __align__(16) char smem[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
@@ -1101,6 +1103,16 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
     if (lane == 0) t = atomicAdd(&ctl->work[pass], 1u);
     t = __shfl_sync(kFull, t, 0);
     if (t >= n) break;
+    if (ready != nullptr) {
+      // streamed input: wait until the copy engine has landed this trace's
+      // group (its flag is written after the group's requests, in order)
+      if (lane == 0) {
+        int g = 0;
+        while (g + 1 < n_groups && t >= group_end[g]) ++g;
+        while (ready[g] == 0u) __nanosleep(2000);
+      }
+      __syncwarp();
+    }
     const int tr = list ? list[t] : (int)t;
     replay_trace(tr, reqs, offs, cfgs, cfg_of, results, timeline, recs, P,
                  dir, kBucket, st, lane);
