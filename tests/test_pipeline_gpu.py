@@ -88,3 +88,18 @@ def test_large_generated_pipeline_vs_oracle(seed, kw, tmp_path):
         got = api.build_sequence(api.analyze(bundle), iterations=it)
         assert [(r.kind.value, r.block_id, r.size, r.virtual_ts)
                 for r in got.requests] == want, it
+
+
+def test_c5_style_trace_vs_oracle():
+    """SURVEY C5 shape (one long trace) at 2e5 events: GPU vs oracle."""
+    from oracle import pipeline as op
+    from paper_2504_03887_b200 import synth_events
+    b = synth_events.generate(6000, iterations=2)
+    assert len(b) > 150_000
+    recs = b.to_json_dict()["traceEvents"]
+    side = {"param_sizes": list(b.metadata.param_sizes),
+            "batch_bytes": list(b.metadata.batch_bytes)}
+    want = op.build_sequence(op.normalize(recs), side, 2)
+    got = api.build_sequence(api.analyze(b), iterations=2)
+    assert [(r.kind.value, r.block_id, r.size, r.virtual_ts)
+            for r in got.requests] == want

@@ -1,0 +1,68 @@
+"""Time the estimator pipeline stages on C5-style traces.
+
+    python tools/bench_pipeline.py --leaves 6000 60000 300000
+
+Per size: events, analyze (host tree + pm_link), build_sequence
+(pm_orchestrate), replay, with events/s; optional --check runs the CPU
+oracle on the same trace and compares the request sequence.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import sys
+import time
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--leaves", type=int, nargs="+", default=[6000])
+    ap.add_argument("--iterations", type=int, default=2)
+    ap.add_argument("--check", action="store_true")
+    args = ap.parse_args()
+    import torch
+    import __graft_entry__
+    __graft_entry__.build()
+    import paper_2504_03887_b200 as api
+    from paper_2504_03887_b200 import synth_events
+    from paper_2504_03887_b200.estimator import replay_sequence
+    torch.cuda.init()
+    # warm the libraries / CUDA context on a tiny trace
+    b0 = synth_events.generate(50, args.iterations)
+    replay_sequence(api.build_sequence(api.analyze(b0), args.iterations),
+                    api.AllocatorConfig())
+    for leaves in args.leaves:
+        t0 = time.perf_counter()
+        b = synth_events.generate(leaves, args.iterations)
+        t1 = time.perf_counter()
+        a = api.analyze(b)
+        t2 = time.perf_counter()
+        seq = api.build_sequence(a, args.iterations)
+        t3 = time.perf_counter()
+        res = replay_sequence(seq, api.AllocatorConfig(), timeline=False)
+        t4 = time.perf_counter()
+        n = len(b)
+        line = {"leaves": leaves, "events": n, "requests": len(seq.requests),
+                "gen_s": t1 - t0, "analyze_s": t2 - t1,
+                "build_sequence_s": t3 - t2, "replay_s": t4 - t3,
+                "pipeline_events_per_s": n / (t4 - t1),
+                "peak_reserved": res.peak_reserved}
+        if args.check:
+            from oracle import pipeline as op
+            recs = b.to_json_dict()["traceEvents"]
+            side = {"param_sizes": list(b.metadata.param_sizes),
+                    "batch_bytes": list(b.metadata.batch_bytes)}
+            tc = time.perf_counter()
+            want = op.build_sequence(op.normalize(recs), side, args.iterations)
+            line["oracle_s"] = time.perf_counter() - tc
+            line["oracle_equal"] = want == [(r.kind.value, r.block_id, r.size,
+                                             r.virtual_ts) for r in seq.requests]
+        print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()
