@@ -261,3 +261,125 @@ def group_memory_events(instants: list[TraceEvent]) -> list[MemoryBlock]:
     z = np.zeros(0, np.int64)
     link = _pipeline.link(z, z, z, st, ad, nb, z, z)
     return blocks_from_link(ad, link)
+
+
+class LayerTreeColumns:
+    """The layer tree of analysis.py:115-182 computed from bundle columns.
+
+    Nearest-layer ancestors come from a vectorised parent-pointer walk
+    (first python id wins; a chain that returns to its own layer or never
+    terminates raises CyclicParentLink, as the reference's seen-set does);
+    children are ordered by (start, event_id); the pre-order walk gives the
+    non-wrapper layers (leaves) the link kernels consume.  LayerNode
+    objects are built only on demand (`tree()`).
+    """
+
+    def __init__(self, bundle):
+        from .trace import EventCategory as EC
+        idx = bundle.indices(EC.PYTHON_FUNCTION)
+        self.bundle = bundle
+        pid = bundle.ints["python_id"][idx]
+        par = bundle.ints["parent_id"][idx]
+        names = bundle.names
+        table = getattr(names, "table", None)
+        if table is not None:  # name-id view: test each distinct name once
+            flag = np.array([_is_layer(t, LAYER_NAME_PREFIXES) for t in table])
+            is_layer = flag[names.ids[idx]]
+        else:
+            is_layer = np.fromiter((_is_layer(names[i], LAYER_NAME_PREFIXES)
+                                    for i in idx.tolist()), bool, len(idx))
+        n = len(idx)
+        from .trace import NONE as NO
+        # first occurrence of every python id
+        valid = pid != NO
+        order = np.argsort(pid, kind="stable")
+        spid = pid[order]
+        first = np.ones(n, bool)
+        first[1:] = spid[1:] != spid[:-1]
+        u_pid = spid[first & (spid != NO)]
+        u_pos = order[first & (spid != NO)]
+        pos = np.searchsorted(u_pid, par)
+        pos = np.clip(pos, 0, max(len(u_pid) - 1, 0))
+        has = (par != NO) & (len(u_pid) > 0)
+        if len(u_pid):
+            has &= u_pid[pos] == par
+        parent_pos = np.where(has, u_pos[pos] if len(u_pid) else -1, -1)
+        del valid
+        lay = np.nonzero(is_layer)[0]
+        anc = np.full(len(lay), -2, np.int64)  # -2 unresolved, -1 root
+        cur = parent_pos[lay]
+        active = np.ones(len(lay), bool)
+        for _ in range(n + 2):
+            if not active.any():
+                break
+            a = np.nonzero(active)[0]
+            c = cur[a]
+            root = c < 0
+            anc[a[root]] = -1
+            active[a[root]] = False
+            a, c = a[~root], c[~root]
+            own = pid[lay[a]]
+            selfhit = (c == lay[a]) | ((own != NO) & (pid[c] == own))
+            if selfhit.any():
+                raise CyclicParentLink("parent chain revisits its own layer")
+            hit = is_layer[c]
+            anc[a[hit]] = c[hit]
+            active[a[hit]] = False
+            cur[a[~hit]] = parent_pos[c[~hit]]
+        else:
+            raise CyclicParentLink("parent chain does not terminate")
+        if active.any():
+            raise CyclicParentLink("parent chain does not terminate")
+        # nodes: the layer events (positions within idx)
+        self.node_event = idx[lay]
+        self.node_start = bundle.start[self.node_event]
+        self.node_end = bundle.end[self.node_event]
+        self.node_name = [names[i] for i in self.node_event.tolist()]
+        lay_index = np.full(n, -1, np.int64)
+        lay_index[lay] = np.arange(len(lay))
+        self.node_parent = np.where(anc >= 0, lay_index[np.maximum(anc, 0)], -1)
+        # children ordered by (start, event_id): sort by (parent, start, id)
+        o = np.lexsort((self.node_event, self.node_start, self.node_parent))
+        self.child_order = o
+        par_sorted = self.node_parent[o]
+        nn = len(lay)
+        counts = np.bincount(par_sorted + 1, minlength=nn + 1)
+        self.child_off = np.zeros(nn + 2, np.int64)
+        np.cumsum(counts, out=self.child_off[1:])
+        self.is_wrapper = counts[1:] > 0
+        # pre-order walk from the synthetic root (parent -1 -> slot 0)
+        walk = []
+        stack = list(reversed(o[self.child_off[0]:self.child_off[1]].tolist()))
+        off = self.child_off
+        while stack:
+            v = stack.pop()
+            walk.append(v)
+            stack.extend(reversed(o[off[v + 1]:off[v + 2]].tolist()))
+        self.walk = np.array(walk, np.int64)
+        leaves = self.walk[~self.is_wrapper[self.walk]] if len(walk) else self.walk
+        self.leaves = leaves
+        self.leaf_start = self.node_start[leaves]
+        self.leaf_end = self.node_end[leaves]
+
+    def tree(self) -> tuple[LayerNode, list[LayerNode]]:
+        """LayerNode objects (root, leaves in walk order)."""
+        nodes = []
+        for k in range(len(self.node_event)):
+            name = self.node_name[k]
+            for prefix in LAYER_NAME_PREFIXES:
+                if name.startswith(prefix):
+                    name = name[len(prefix):]
+                    break
+            nodes.append(LayerNode(name=name, start_ts=int(self.node_start[k]),
+                                   end_ts=int(self.node_end[k]),
+                                   event_id=int(self.node_event[k]),
+                                   is_wrapper=bool(self.is_wrapper[k])))
+        root = LayerNode(name="<root>", start_ts=0, end_ts=0, is_wrapper=True)
+        o, off = self.child_order, self.child_off
+        root.children = [nodes[v] for v in o[off[0]:off[1]].tolist()]
+        for k, node in enumerate(nodes):
+            node.children = [nodes[v] for v in o[off[k + 1]:off[k + 2]].tolist()]
+        if root.children:
+            root.start_ts = min(c.start_ts for c in root.children)
+            root.end_ts = max(c.end_ts for c in root.children)
+        return root, [nodes[v] for v in self.leaves.tolist()]

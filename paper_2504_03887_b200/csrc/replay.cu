@@ -48,7 +48,7 @@ Layout layout_for(int64_t total_events, int64_t max_trace_events,
   Layout L;
   size_t off = align_up(sizeof(pmb::Ctl), 256);
   L.retry_list = off;
-  off = align_up(off + 2 * sizeof(int32_t) * (size_t)(n_traces > 0 ? n_traces : 1),
+  off = align_up(off + 3 * sizeof(int32_t) * (size_t)(n_traces > 0 ? n_traces : 1),
                  256);
   const int64_t mx = max_trace_events > 0 ? max_trace_events : 1;
   L.nbmax_g = (int)(mx / 8 + 4);
@@ -68,6 +68,8 @@ struct Occupancy {
   size_t smem = 0;
   int per_sm1 = 0;  // tier-1 retry kernel
   size_t smem1 = 0;
+  int nbmax2 = 0;   // tier-2: one warp with a shared-memory directory
+  size_t smem2 = 0;
 };
 
 constexpr int kTier1Warps = 8;  // tier 1: a dedicated 32-bucket pool per warp
@@ -125,6 +127,13 @@ int query_occupancy(Occupancy* out) {
     rc = setup_kernel<kTier1Warps>(optin, kTier1Warps * 32, &b1, &o.smem1,
                                    &o.per_sm1);
     if (rc != PM_SUCCESS) return rc;
+    o.nbmax2 = (int)(((size_t)optin - 1024) / (kBucket_host * 24 + 32));
+    while (o.nbmax2 > 8 && pmb::gmem_warp_bytes(o.nbmax2) > (size_t)optin) --o.nbmax2;
+    o.smem2 = pmb::gmem_warp_bytes(o.nbmax2);
+    e = cudaFuncSetAttribute(pmb::replay_dirmem_kernel<1, true>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)o.smem2);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute tier 2");
     cached = o;
     cached_dev = dev;
   }
@@ -247,12 +256,22 @@ int replay_batch_impl(const pm_req_t* reqs, const int64_t* trace_offsets,
           ctl, 1, list1, 0, list2, kTier1Warps * 32, nullptr, 0, nullptr);
   e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "replay tier-1 launch");
-  pmb::replay_gpool_kernel<kRetryWarps>
-      <<<L.retry_warps / kRetryWarps, kRetryWarps * 32, 0, stream>>>(
-          reqs, trace_offsets, cfgs, cfg_of_trace, results, timeline, recs,
-          ctl, list2, gpool, L.nbmax_g);
+  {
+    int32_t* list3 = retry_list + 2 * (size_t)n_traces;
+    long long grid2 = occ.sms;
+    if (n_traces < grid2) grid2 = n_traces;
+    pmb::replay_dirmem_kernel<1, true><<<(unsigned)grid2, 32, occ.smem2, stream>>>(
+        reqs, trace_offsets, cfgs, cfg_of_trace, results, timeline, recs, ctl,
+        2, list2, list3, nullptr, occ.nbmax2);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "replay tier-2 launch");
+    pmb::replay_dirmem_kernel<kRetryWarps, false>
+        <<<L.retry_warps / kRetryWarps, kRetryWarps * 32, 0, stream>>>(
+            reqs, trace_offsets, cfgs, cfg_of_trace, results, timeline, recs,
+            ctl, 3, list3, nullptr, gpool, L.nbmax_g);
+  }
   e = cudaGetLastError();
-  if (e != cudaSuccess) return cuda_fail(e, "replay_gpool_kernel launch");
+  if (e != cudaSuccess) return cuda_fail(e, "replay tier-3 launch");
   return PM_SUCCESS;
 }
 

@@ -242,13 +242,15 @@ struct DirReg {
   __device__ __forceinline__ bool full() const { return nb >= nbmax; }
 };
 
-// Directory in memory (retry kernel, any number of buckets).
+// Directory in memory (retry tiers, any number of buckets): sorted bounds
+// with a 32-ary warp-cooperative search and a physical -> position map.
 struct DirMem {
   u64* dkey;
   u64* daddr;
   int* dphys;
   int* cnt;     // by physical bucket
   int* pstack;  // free physical buckets
+  int* pos;     // by physical bucket: directory position
   int nb, ptop, nbmax, lane;
 
   __device__ __forceinline__ void init(int nbmax_, int lane_) {
@@ -259,16 +261,23 @@ struct DirMem {
     __syncwarp();
     ptop = nbmax;
   }
+  // last position whose bound <= (k, a): each round 32 lanes probe evenly
+  // spaced positions of the live range, shrinking it 32x
   __device__ __forceinline__ int find(u64 k, u64 a) const {
-    int d = 0;
-    for (int base = 0; base < nb; base += 32) {
-      const int e = base + lane;
-      const bool pr = e < nb && dir_le(dkey[e], daddr[e], k, a);
+    int lo = 0, hi = nb;  // answer in [lo, hi), bound[lo] <= (k, a)
+    while (hi - lo > 32) {
+      const int step = (hi - lo + 31) / 32;
+      const int e = lo + lane * step;
+      const bool pr = e < hi && dir_le(dkey[e], daddr[e], k, a);
       const unsigned m = __ballot_sync(kFull, pr);
-      if (m) d = base + 31 - __clz(m);
-      if (m != kFull) break;
+      const int t = 31 - __clz(m);  // lane 0 probes lo, always true
+      lo = lo + t * step;
+      hi = min(lo + step, hi);
     }
-    return d;
+    const int e = lo + lane;
+    const bool pr = e < hi && dir_le(dkey[e], daddr[e], k, a);
+    const unsigned m = __ballot_sync(kFull, pr);
+    return m ? lo + 31 - __clz(m) : lo;
   }
   __device__ __forceinline__ int phys(int d) const { return dphys[d]; }
   __device__ __forceinline__ int count(int d) const { return cnt[dphys[d]]; }
@@ -288,14 +297,7 @@ struct DirMem {
     cnt[p] = c;
     __syncwarp();
   }
-  __device__ __forceinline__ int pos_of_phys(int p) const {
-    for (int base = 0; base < nb; base += 32) {
-      const int e = base + lane;
-      const unsigned m = __ballot_sync(kFull, e < nb && dphys[e] == p);
-      if (m) return base + __ffs(m) - 1;
-    }
-    return -1;
-  }
+  __device__ __forceinline__ int pos_of_phys(int p) const { return pos[p]; }
   __device__ __forceinline__ int mergeable() const {
     for (int base = 0; base < nb - 1; base += 32) {
       const int x = base + lane;
@@ -322,14 +324,15 @@ struct DirMem {
         dkey[e + 1] = xk;
         daddr[e + 1] = xa;
         dphys[e + 1] = xp;
+        pos[xp] = e + 1;
       }
       __syncwarp();
     }
-    __syncwarp();
     dkey[d] = k;
     daddr[d] = a;
     dphys[d] = p;
     cnt[p] = c;
+    pos[p] = d;
     __syncwarp();
     nb += 1;
   }
@@ -349,6 +352,7 @@ struct DirMem {
         dkey[e - 1] = xk;
         daddr[e - 1] = xa;
         dphys[e - 1] = xp;
+        pos[xp] = e - 1;
       }
       __syncwarp();
     }
@@ -1029,9 +1033,9 @@ __device__ __forceinline__ void replay_trace(
 // ---- kernels -------------------------------------------------------------------
 
 struct Ctl {
-  unsigned work[3];   // work counters: main pass, tier-1 retry, tier-2 retry
-  unsigned n_list[3]; // traces queued for tier 1 / tier 2 (index 1, 2)
-  unsigned pad[58];
+  unsigned work[4];   // work counters: main pass, tiers 1, 2 and 3
+  unsigned n_list[4]; // traces queued for tier 1 / 2 / 3 (index 1..3)
+  unsigned pad[56];
 };
 
 // Shared-memory layout of the main kernel (per CTA): the bucket pool
@@ -1044,7 +1048,7 @@ __host__ __device__ __forceinline__ size_t smem_cta_bytes(int buckets,
          (size_t)((buckets + 31) / 32) * 4;
 }
 __host__ __device__ __forceinline__ size_t gmem_warp_bytes(int nbmax) {
-  return ((size_t)nbmax * kBucket * 24 + 32 * 24 + (size_t)nbmax * 28 + 255) /
+  return ((size_t)nbmax * kBucket * 24 + 32 * 24 + (size_t)nbmax * 32 + 255) /
          256 * 256;
 }
 
@@ -1124,51 +1128,61 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
   }
 }
 
-// Tier 2 -- traces whose free blocks outgrew even a dedicated 32-bucket
-// shared-memory pool: the same replay with the entries and the directory in
-// a per-warp HBM region sized for the longest
-// trace (free blocks never exceed live allocations + live segments <= 2 x
-// requests, and with every adjacent bucket pair holding > 32 entries a
-// directory of n/8+4 buckets always has room).
-template <int WARPS>
+// Tiers 2 and 3 -- traces whose free blocks outgrew a dedicated 32-bucket
+// register directory: the same replay with a memory-resident directory.
+// Tier 2 gives one warp a whole SM's shared memory (~290 buckets); tier 3
+// puts the entries and the directory in a per-warp HBM region sized for the
+// longest trace (free blocks never exceed live allocations + live segments
+// <= 2 x requests, and with every adjacent bucket pair holding > 32 entries
+// a directory of n/8+4 buckets always has room).
+template <int WARPS, bool SMEM>
 __global__ void __launch_bounds__(WARPS * 32, 1)
-    replay_gpool_kernel(const pm_req_t* __restrict__ reqs,
-                        const int64_t* __restrict__ offs,
-                        const pm_cfg_t* __restrict__ cfgs,
-                        const int32_t* __restrict__ cfg_of,
-                        pm_result_t* __restrict__ results,
-                        int64_t* __restrict__ timeline,
-                        u64* recs, Ctl* ctl,
-                        const int32_t* __restrict__ retry_list,
-                        char* __restrict__ gpool, int nbmax_g) {
+    replay_dirmem_kernel(const pm_req_t* __restrict__ reqs,
+                         const int64_t* __restrict__ offs,
+                         const pm_cfg_t* __restrict__ cfgs,
+                         const int32_t* __restrict__ cfg_of,
+                         pm_result_t* __restrict__ results,
+                         int64_t* __restrict__ timeline, u64* recs, Ctl* ctl,
+                         int pass, const int32_t* __restrict__ list,
+                         int32_t* __restrict__ overflow_list,
+                         char* __restrict__ gpool, int nbmax) {
+  extern __shared__ __align__(16) char smem[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
   const long long gw = (long long)blockIdx.x * WARPS + wib;
-  char* base = gpool + (size_t)gw * gmem_warp_bytes(nbmax_g);
+  char* base = SMEM ? smem + (size_t)wib * gmem_warp_bytes(nbmax)
+                    : gpool + (size_t)gw * gmem_warp_bytes(nbmax);
   Pool P;
   Stage st;
-  carve_pool(base, nbmax_g, P);
-  carve_stage(base + (size_t)nbmax_g * kBucket * 24, st);
+  carve_pool(base, nbmax, P);
+  carve_stage(base + (size_t)nbmax * kBucket * 24, st);
   DirMem dir;
   {
-    u64* q = reinterpret_cast<u64*>(base + (size_t)nbmax_g * kBucket * 24 +
+    u64* q = reinterpret_cast<u64*>(base + (size_t)nbmax * kBucket * 24 +
                                     32 * 24);
     dir.dkey = q;
-    dir.daddr = q + nbmax_g;
-    int* ip = reinterpret_cast<int*>(q + 2 * (size_t)nbmax_g);
+    dir.daddr = q + nbmax;
+    int* ip = reinterpret_cast<int*>(q + 2 * (size_t)nbmax);
     dir.dphys = ip;
-    dir.cnt = ip + nbmax_g;
-    dir.pstack = ip + 2 * nbmax_g;
+    dir.cnt = ip + nbmax;
+    dir.pstack = ip + 2 * nbmax;
+    dir.pos = ip + 3 * nbmax;
   }
-  const unsigned n_retry = ctl->n_list[2];
+  const unsigned n = ctl->n_list[pass];
   for (;;) {
     unsigned t = 0;
-    if (lane == 0) t = atomicAdd(&ctl->work[2], 1u);
+    if (lane == 0) t = atomicAdd(&ctl->work[pass], 1u);
     t = __shfl_sync(kFull, t, 0);
-    if (t >= n_retry) break;
-    const int tr = retry_list[t];
+    if (t >= n) break;
+    const int tr = list[t];
     replay_trace(tr, reqs, offs, cfgs, cfg_of, results, timeline, recs, P,
-                 dir, nbmax_g, st, lane);
+                 dir, nbmax, st, lane);
+    __syncwarp();
+    if (overflow_list != nullptr && lane == 0 &&
+        results[tr].status == PM_POOL_OVERFLOW) {
+      const unsigned k = atomicAdd(&ctl->n_list[pass + 1], 1u);
+      overflow_list[k] = tr;
+    }
   }
 }
 

@@ -12,18 +12,18 @@ packed replay records so the estimator feeds the replay kernel directly.
 
 from __future__ import annotations
 
-from dataclasses import dataclass, field
+from dataclasses import dataclass
 from enum import Enum
 
 import numpy as np
 
 from . import _pipeline
-from .analysis import (AnnotationMarker, BlockRole, LayerNode, MarkerKind,
-                       MemoryBlock, OperatorNode, ROLE_OF_CODE,
-                       blocks_from_link, build_layer_tree, extract_markers,
+from .analysis import (AnnotationMarker, BlockRole, LayerNode,
+                       LayerTreeColumns, MarkerKind, MemoryBlock, OperatorNode,
+                       ROLE_OF_CODE, blocks_from_link, extract_markers,
                        roots_from_link)
 from .errors import MissingBatchBytes, NoGradientBlocks, NoIterations
-from .linking import LayerMemoryProfile, non_wrapper_layers, profiles_from_link
+from .linking import LayerMemoryProfile, profiles_from_link
 from .trace import EventCategory, NONE, TraceBundle
 
 
@@ -49,14 +49,73 @@ class MemoryRequest:
                 "virtual_ts": self.virtual_ts, "stream": self.stream}
 
 
-@dataclass
 class RequestSequence:
-    """orchestration.py:70-87, plus the packed replay records."""
+    """orchestration.py:70-87.  Built by build_sequence from the device's
+    ordered arrays; `requests` and `phase_tags` materialise on first use
+    (the estimator reads only the arrays and the packed replay records)."""
 
-    requests: list[MemoryRequest]
-    iteration_boundaries: list[int]
-    phase_tags: dict
-    packed: np.ndarray | None = field(default=None, repr=False, compare=False)
+    def __init__(self, requests=None, iteration_boundaries=None,
+                 phase_tags=None, packed=None, arrays=None):
+        self._requests = requests
+        self.iteration_boundaries = list(iteration_boundaries or [])
+        self._phase_tags = phase_tags
+        self.packed = packed
+        self._arrays = arrays
+
+    def __len__(self) -> int:
+        if self._requests is not None:
+            return len(self._requests)
+        return int(self._arrays["n"])
+
+    @property
+    def requests(self) -> list[MemoryRequest]:
+        if self._requests is None:
+            a = self._arrays
+            kinds = (RequestKind.ALLOC, RequestKind.FREE)
+            self._requests = [
+                MemoryRequest(seq_no=i, kind=kinds[k], block_id=_block_id(t, x, y),
+                              size=sz, virtual_ts=v)
+                for i, (t, x, y, k, sz, v) in enumerate(zip(
+                    a["tag"].tolist(), a["a"].tolist(), a["b"].tolist(),
+                    a["kind"].tolist(), a["size"].tolist(), a["vts"].tolist()))]
+        return self._requests
+
+    @property
+    def phase_tags(self) -> dict:
+        if self._phase_tags is None:
+            a = self._arrays
+            tags: dict = {}
+            for i in range(a["n_model"]):
+                tags[f"model:{i}"] = BlockRole.MODEL
+            for it, j in a["batch_ids"]:
+                tags[f"batch:{it}:{j}"] = BlockRole.BATCH
+            order = np.argsort(a["raw"], kind="stable")
+            tg, x, y, rl, k = (a["tag"][order], a["a"][order], a["b"][order],
+                               a["role"][order], a["kind"][order])
+            sel = (tg >= 2) & (k == 0)
+            for t, xx, yy, r in zip(tg[sel].tolist(), x[sel].tolist(),
+                                    y[sel].tolist(), rl[sel].tolist()):
+                tags[_block_id(t, xx, yy)] = ROLE_OF_CODE[r]
+            self._phase_tags = tags
+        return self._phase_tags
+
+    def breakdown(self) -> dict[str, int]:
+        """Sum of ALLOC sizes per role value (estimator.py:160-164)."""
+        if self._arrays is None:
+            out: dict[str, int] = {}
+            for r in self.requests:
+                if r.kind is RequestKind.ALLOC:
+                    role = self.phase_tags[r.block_id].value
+                    out[role] = out.get(role, 0) + r.size
+            return out
+        a = self._arrays
+        alloc = a["kind"] == 0
+        roles = a["role"][alloc]
+        sizes = a["size"][alloc]
+        out = {}
+        for code in np.unique(roles).tolist():
+            out[ROLE_OF_CODE[code].value] = int(sizes[roles == code].sum())
+        return out
 
     def to_json_dict(self) -> dict:
         return {
@@ -71,18 +130,57 @@ class RequestSequence:
                 for r in self.requests]
 
 
-@dataclass
 class AnalyzedTrace:
-    """orchestration.py:90-104"""
+    """orchestration.py:90-104.  Structural views of one bundle; the object
+    views (layer_tree, operator_roots, blocks, profiles) materialise from
+    the device's columnar link result on first access."""
 
-    bundle: TraceBundle
-    layer_tree: LayerNode
-    operator_roots: list[OperatorNode]
-    markers: list[AnnotationMarker]
-    blocks: list[MemoryBlock]
-    profiles: dict
-    # device-side link result (block roles incl. the gradient tags)
-    _link: object = field(default=None, repr=False, compare=False)
+    def __init__(self, bundle, tree_cols, markers, link, op_idx):
+        self.bundle = bundle
+        self.markers = markers
+        self._tree = tree_cols
+        self._link = link
+        self._ops = op_idx
+        self._objects = None
+        self._final = None  # (roles, frees) of the last build_sequence
+
+    def _materialise(self):
+        if self._objects is None:
+            root, leaves = self._tree.tree()
+            names = self.bundle.names
+            op_names = [names[i] for i in self._ops.tolist()]
+            roots = roots_from_link(op_names, None, None, self._link)
+            inst = self.bundle.indices(EventCategory.CPU_INSTANT_EVENT)
+            blocks = blocks_from_link(self.bundle.ints["addr"][inst], self._link)
+            profiles = profiles_from_link(leaves, roots, blocks, self._link)
+            self._objects = (root, roots, blocks, profiles)
+            if self._final is not None:
+                self._apply_final()
+        return self._objects
+
+    @property
+    def layer_tree(self) -> LayerNode:
+        return self._materialise()[0]
+
+    @property
+    def operator_roots(self) -> list[OperatorNode]:
+        return self._materialise()[1]
+
+    @property
+    def blocks(self) -> list[MemoryBlock]:
+        return self._materialise()[2]
+
+    @property
+    def profiles(self) -> dict:
+        return self._materialise()[3]
+
+    def _apply_final(self):
+        """build_sequence mutates the analyzed blocks in place, like the
+        reference (orchestration.py:222-223, 197)."""
+        roles, frees = self._final
+        for blk, rc, fr in zip(self._objects[2], roles.tolist(), frees.tolist()):
+            blk.role = ROLE_OF_CODE[rc]
+            blk.free_time = None if fr == NONE else fr
 
     def steps(self) -> list[AnnotationMarker]:
         return sorted((m for m in self.markers
@@ -92,25 +190,17 @@ class AnalyzedTrace:
 
 def analyze(bundle: TraceBundle) -> AnalyzedTrace:
     """Build every structural view and link them (orchestration.py:107-116)."""
-    tree = build_layer_tree(bundle.by_category(EventCategory.PYTHON_FUNCTION))
+    tree = LayerTreeColumns(bundle)
     ops = bundle.indices(EventCategory.CPU_OP)
     inst = bundle.indices(EventCategory.CPU_INSTANT_EVENT)
     markers = extract_markers(bundle.by_category(EventCategory.USER_ANNOTATION))
-    leaves = non_wrapper_layers(tree)
     seq = bundle.ints["sequence_number"][ops]
     seq = np.where(seq == NONE, -1, seq)
     lk = _pipeline.link(bundle.start[ops], bundle.end[ops], seq,
                         bundle.start[inst], bundle.ints["addr"][inst],
-                        bundle.ints["nbytes"][inst],
-                        np.array([n.start_ts for n in leaves], np.int64),
-                        np.array([n.end_ts for n in leaves], np.int64))
-    op_names = [bundle.names[i] for i in ops.tolist()]
-    roots = roots_from_link(op_names, None, None, lk)
-    blocks = blocks_from_link(bundle.ints["addr"][inst], lk)
-    profiles = profiles_from_link(leaves, roots, blocks, lk)
-    return AnalyzedTrace(bundle=bundle, layer_tree=tree, operator_roots=roots,
-                         markers=markers, blocks=blocks, profiles=profiles,
-                         _link=lk)
+                        bundle.ints["nbytes"][inst], tree.leaf_start,
+                        tree.leaf_end)
+    return AnalyzedTrace(bundle, tree, markers, lk, ops)
 
 
 def _block_id(tag: int, a: int, b: int):
@@ -173,8 +263,7 @@ def build_sequence(analyzed: AnalyzedTrace, iterations: int = 2,
             bi += [step.iteration_index] * 2
             bj += [j, j]
 
-    blocks = analyzed.blocks
-    nb = len(blocks)
+    nb = int(lk.n_blocks)
     role_codes = lk.b_role if nb else np.zeros(0, np.int32)
     o = _pipeline.orchestrate(
         lk.b_alloc, lk.b_size, lk.b_free, role_codes,
@@ -190,29 +279,12 @@ def build_sequence(analyzed: AnalyzedTrace, iterations: int = 2,
         raise MissingBatchBytes("sidecar provides no batch tensor sizes")
 
     # the reference mutates the analyzed blocks in place
-    for blk, rc, fr in zip(blocks, o.fb_role.tolist(), o.fb_free.tolist()):
-        blk.role = ROLE_OF_CODE[rc]
-        blk.free_time = None if fr == NONE else fr
-
-    requests = []
-    phase_tags: dict = {}
-    kinds = (RequestKind.ALLOC, RequestKind.FREE)
-    for i in range(o.n_model):
-        phase_tags[f"model:{i}"] = BlockRole.MODEL
-    for it, j in zip(bi[::2], bj[::2]):
-        phase_tags[f"batch:{it}:{j}"] = BlockRole.BATCH
-    # chosen blocks then clones, in raw (emission) order
-    raw_order = np.argsort(o.raw, kind="stable")
-    tags, aa, bb, roles, kk = (o.tag.tolist(), o.a.tolist(), o.b.tolist(),
-                               o.role.tolist(), o.kind.tolist())
-    for i in raw_order.tolist():
-        if tags[i] >= 2 and kk[i] == 0:
-            phase_tags[_block_id(tags[i], aa[i], bb[i])] = ROLE_OF_CODE[roles[i]]
-    for seq_no, (t, a, b, kind, size, vts) in enumerate(zip(
-            tags, aa, bb, kk, o.size.tolist(), o.vts.tolist())):
-        requests.append(MemoryRequest(seq_no=seq_no, kind=kinds[kind],
-                                      block_id=_block_id(t, a, b), size=size,
-                                      virtual_ts=vts))
+    analyzed._final = (o.fb_role, o.fb_free)
+    if analyzed._objects is not None:
+        analyzed._apply_final()
+    arrays = {"n": o.n, "n_model": o.n_model, "kind": o.kind, "size": o.size,
+              "vts": o.vts, "tag": o.tag, "a": o.a, "b": o.b, "role": o.role,
+              "raw": o.raw, "batch_ids": list(zip(bi[::2], bj[::2]))}
     boundaries = [w[0] for w in windows]
     end = windows[-1][1]
     if clones:
@@ -220,8 +292,8 @@ def build_sequence(analyzed: AnalyzedTrace, iterations: int = 2,
             boundaries.append(windows[-1][0] + width * c)
         end = windows[-1][0] + width * (clones + 1)
     boundaries.append(end)
-    return RequestSequence(requests=requests, iteration_boundaries=boundaries,
-                           phase_tags=phase_tags, packed=o.packed)
+    return RequestSequence(iteration_boundaries=boundaries, packed=o.packed,
+                           arrays=arrays)
 
 
 __all__ = ["AnalyzedTrace", "MemoryRequest", "RequestKind", "RequestSequence",

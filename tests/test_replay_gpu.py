@@ -326,3 +326,20 @@ def test_many_traces_per_warp_vs_oracle(monkeypatch):
     want, tl_ref = oracle.replay_batch(r2, o2, c2, f2, timeline=True)
     assert_same(got, want)
     assert (tl == tl_ref).all()
+
+
+def test_hbm_tier_vs_oracle():
+    # 10k non-adjacent free blocks outgrow the shared-memory tiers (~9k
+    # entries) and land in the HBM-directory tier
+    seq = [alloc(i, i, 512) for i in range(20_000)]
+    seq += [free(20_000 + k, 2 * k) for k in range(10_000)]
+    seq += [alloc(30_000 + k, 50_000 + k, 512) for k in range(3_000)]
+    p = pack_trace(seq)
+    offs = np.array([0, len(seq)], dtype=np.int64)
+    got, tl = _native.replay_host(p.reqs, offs, cfg_record(AllocatorConfig()),
+                                  None, True)
+    want, tl_ref = oracle.replay_batch(p.reqs, offs, cfg_record(AllocatorConfig()),
+                                       timeline=True)
+    assert int(want[0]["max_free_blocks"]) >= 10_000
+    assert_same(got, want)
+    assert (tl == tl_ref).all()
