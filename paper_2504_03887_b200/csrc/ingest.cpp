@@ -1,0 +1,738 @@
+// Native trace ingest and config digest.
+//
+// pm_ingest_json: chrome-trace JSON text -> the columns the reference's
+// parse_trace builds (reference pkg/src/peakmem/trace.py:155-238): raw ts,
+// dur, category, the seven integer args fields (INT64_MIN = None) and the
+// names (interned: an id per event into a table of distinct names, UTF-8
+// blob + code-point offsets), in FILE order, metadata records
+// dropped, instants without a usable Addr/Bytes pair dropped.  It handles
+// the common case exactly (numbers parsed with correctly rounded strtod,
+// integers exact, floats truncated like int(), last duplicate key wins, JSON
+// escapes decoded) and returns PM_INGEST_UNSUPPORTED for anything outside it
+// (string-typed numbers, NaN / Infinity, non-object args, errors the
+// reference reports with a message) so the caller's Python reader can take
+// over with the reference's exact semantics.
+//
+// pm_bundle_digest: SHA-256 of json.dumps(payload, sort_keys=True,
+// separators=(",", ":")) for the estimator's config digest
+// (estimator.py:189-202; TraceBundle.to_json_dict, trace.py:116-143),
+// streamed from the columns -- ensure_ascii escaping included.
+
+#include <cerrno>
+#include <charconv>
+#include <cmath>
+#include <cstdio>
+#include <cstdint>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include <openssl/evp.h>
+
+#include "../../include/peakmem_ingest.h"
+
+namespace {
+
+constexpr int64_t kNone = INT64_MIN;
+enum { PM_INGEST_OK = 0 };
+enum Cat { C_PF = 0, C_OP = 1, C_UA = 2, C_IN = 3, C_OTHER = 4 };
+enum Field { F_PID = 0, F_PAR, F_SEQ, F_ADDR, F_BYTES, F_TA, F_TR, F_N };
+
+thread_local std::string g_err;
+
+struct Cols {
+  std::vector<double> ts, dur;
+  std::vector<int8_t> cat;
+  std::vector<int64_t> ints[F_N];
+  std::vector<int32_t> name_id;    // per event, into the table below
+  std::unordered_map<std::string, int32_t> intern;
+  std::string names;               // distinct names, UTF-8
+  std::vector<int64_t> name_off;   // code-point offsets, n_names+1
+  int64_t dropped = 0;
+  int64_t cp_total = 0;
+};
+
+// ---- JSON scanning -----------------------------------------------------------
+
+struct Unsupported {};
+
+struct Parser {
+  const char* p;
+  const char* end;
+
+  void ws() {
+    while (p < end && (*p == ' ' || *p == '\n' || *p == '\r' || *p == '\t')) ++p;
+  }
+  char peek() {
+    ws();
+    if (p >= end) throw Unsupported();
+    return *p;
+  }
+  void expect(char c) {
+    if (peek() != c) throw Unsupported();
+    ++p;
+  }
+  static void put_utf8(std::string& out, uint32_t cp) {
+    if (cp < 0x80) {
+      out += (char)cp;
+    } else if (cp < 0x800) {
+      out += (char)(0xC0 | (cp >> 6));
+      out += (char)(0x80 | (cp & 0x3F));
+    } else if (cp < 0x10000) {
+      out += (char)(0xE0 | (cp >> 12));
+      out += (char)(0x80 | ((cp >> 6) & 0x3F));
+      out += (char)(0x80 | (cp & 0x3F));
+    } else {
+      out += (char)(0xF0 | (cp >> 18));
+      out += (char)(0x80 | ((cp >> 12) & 0x3F));
+      out += (char)(0x80 | ((cp >> 6) & 0x3F));
+      out += (char)(0x80 | (cp & 0x3F));
+    }
+  }
+  uint32_t hex4() {
+    if (end - p < 4) throw Unsupported();
+    uint32_t v = 0;
+    for (int i = 0; i < 4; ++i) {
+      const char c = *p++;
+      v <<= 4;
+      if (c >= '0' && c <= '9') v |= c - '0';
+      else if (c >= 'a' && c <= 'f') v |= c - 'a' + 10;
+      else if (c >= 'A' && c <= 'F') v |= c - 'A' + 10;
+      else throw Unsupported();
+    }
+    return v;
+  }
+  // string -> UTF-8 (lone surrogates unsupported)
+  std::string str() {
+    expect('"');
+    std::string out;
+    const char* run = p;
+    while (true) {
+      if (p >= end) throw Unsupported();
+      const unsigned char c = (unsigned char)*p;
+      if (c == '"') {
+        out.append(run, p - run);
+        ++p;
+        return out;
+      }
+      if (c < 0x20) throw Unsupported();
+      if (c != '\\') {
+        ++p;
+        continue;
+      }
+      out.append(run, p - run);
+      ++p;
+      if (p >= end) throw Unsupported();
+      const char e = *p++;
+      switch (e) {
+        case '"': out += '"'; break;
+        case '\\': out += '\\'; break;
+        case '/': out += '/'; break;
+        case 'b': out += '\b'; break;
+        case 'f': out += '\f'; break;
+        case 'n': out += '\n'; break;
+        case 'r': out += '\r'; break;
+        case 't': out += '\t'; break;
+        case 'u': {
+          uint32_t cp = hex4();
+          if (cp >= 0xD800 && cp < 0xDC00) {
+            if (end - p < 6 || p[0] != '\\' || p[1] != 'u') throw Unsupported();
+            p += 2;
+            const uint32_t lo = hex4();
+            if (lo < 0xDC00 || lo >= 0xE000) throw Unsupported();
+            cp = 0x10000 + ((cp - 0xD800) << 10) + (lo - 0xDC00);
+          } else if (cp >= 0xDC00 && cp < 0xE000) {
+            throw Unsupported();
+          }
+          put_utf8(out, cp);
+          break;
+        }
+        default: throw Unsupported();
+      }
+      run = p;
+    }
+  }
+  // object key without copying when it has no escapes; escaped keys decode
+  // into `scratch`
+  std::pair<const char*, size_t> key(std::string& scratch) {
+    expect('"');
+    const char* s = p;
+    while (p < end && *p != '"' && *p != '\\' && (unsigned char)*p >= 0x20) ++p;
+    if (p < end && *p == '"') {
+      ++p;
+      return {s, (size_t)(p - 1 - s)};
+    }
+    p = s - 1;
+    scratch = str();
+    return {scratch.data(), scratch.size()};
+  }
+  // number token: kind 1 = integer, 2 = float
+  int number(const char** s, const char** e) {
+    ws();
+    *s = p;
+    if (p < end && *p == '-') ++p;
+    if (p >= end || !(*p >= '0' && *p <= '9')) throw Unsupported();
+    if (*p == '0' && p + 1 < end && p[1] >= '0' && p[1] <= '9')
+      throw Unsupported();  // leading zero: invalid JSON
+    int kind = 1;
+    while (p < end && *p >= '0' && *p <= '9') ++p;
+    if (p < end && *p == '.') {
+      kind = 2;
+      ++p;
+      if (p >= end || !(*p >= '0' && *p <= '9')) throw Unsupported();
+      while (p < end && *p >= '0' && *p <= '9') ++p;
+    }
+    if (p < end && (*p == 'e' || *p == 'E')) {
+      kind = 2;
+      ++p;
+      if (p < end && (*p == '+' || *p == '-')) ++p;
+      if (p >= end || !(*p >= '0' && *p <= '9')) throw Unsupported();
+      while (p < end && *p >= '0' && *p <= '9') ++p;
+    }
+    *e = p;
+    return kind;
+  }
+  void literal(const char* w) {
+    const size_t n = strlen(w);
+    if ((size_t)(end - p) < n || memcmp(p, w, n) != 0) throw Unsupported();
+    p += n;
+  }
+  void skip() {
+    const char c = peek();
+    if (c == '{') {
+      ++p;
+      if (peek() == '}') { ++p; return; }
+      std::string scratch;
+      while (true) {
+        key(scratch);
+        expect(':');
+        skip();
+        const char d = peek();
+        ++p;
+        if (d == '}') return;
+        if (d != ',') throw Unsupported();
+      }
+    } else if (c == '[') {
+      ++p;
+      if (peek() == ']') { ++p; return; }
+      while (true) {
+        skip();
+        const char d = peek();
+        ++p;
+        if (d == ']') return;
+        if (d != ',') throw Unsupported();
+      }
+    } else if (c == '"') {
+      str();
+    } else if (c == 't') {
+      literal("true");
+    } else if (c == 'f') {
+      literal("false");
+    } else if (c == 'n') {
+      literal("null");
+    } else {
+      const char *s, *e;
+      number(&s, &e);
+    }
+  }
+};
+
+// A scalar JSON value as the reference sees it after json.loads.
+struct Val {
+  enum T { ABSENT, NUL, INT, FLT, STR, TRUE_, FALSE_, OTHER } t = ABSENT;
+  int64_t i = 0;
+  double f = 0;
+  std::string s;
+};
+
+Val scalar(Parser& P) {
+  Val v;
+  const char c = P.peek();
+  if (c == '"') {
+    v.t = Val::STR;
+    v.s = P.str();
+  } else if (c == 'n') {
+    P.literal("null");
+    v.t = Val::NUL;
+  } else if (c == 't') {
+    P.literal("true");
+    v.t = Val::TRUE_;
+  } else if (c == 'f') {
+    P.literal("false");
+    v.t = Val::FALSE_;
+  } else if (c == '{' || c == '[') {
+    P.skip();
+    v.t = Val::OTHER;
+  } else {
+    const char *s, *e;
+    const int kind = P.number(&s, &e);
+    if (kind == 1) {
+      const bool neg = *s == '-';
+      uint64_t mag = 0;
+      for (const char* q = s + neg; q < e; ++q) {
+        if (__builtin_mul_overflow(mag, (uint64_t)10, &mag) ||
+            __builtin_add_overflow(mag, (uint64_t)(*q - '0'), &mag))
+          throw Unsupported();  // Python int beyond int64
+      }
+      if (mag > (neg ? (uint64_t)1 << 63 : (uint64_t)INT64_MAX)) throw Unsupported();
+      v.t = Val::INT;
+      v.i = neg ? (int64_t)(0 - mag) : (int64_t)mag;
+      v.f = (double)v.i;  // float(int): round to nearest even
+    } else {
+      v.t = Val::FLT;
+      // correctly rounded like Python's float(); overflow / underflow ->
+      // out_of_range -> the Python reader decides
+      const auto r = std::from_chars(s, e, v.f);
+      if (r.ec != std::errc() || r.ptr != e || !std::isfinite(v.f))
+        throw Unsupported();
+    }
+  }
+  return v;
+}
+
+// _as_int (trace.py:140-146): None -> None, int(value) otherwise
+int64_t as_int(const Val& v) {
+  switch (v.t) {
+    case Val::ABSENT:
+    case Val::NUL: return kNone;
+    case Val::INT:
+      if (v.i == kNone) throw Unsupported();
+      return v.i;
+    case Val::TRUE_: return 1;
+    case Val::FALSE_: return 0;
+    case Val::FLT: {
+      const double t = std::trunc(v.f);
+      if (!(t > -9.2e18 && t < 9.2e18)) throw Unsupported();
+      return (int64_t)t;
+    }
+    default: throw Unsupported();  // strings / containers: Python path
+  }
+}
+
+bool truthy(const Val& v) {  // `x or 0`
+  switch (v.t) {
+    case Val::INT: return v.i != 0;
+    case Val::FLT: return v.f != 0.0;
+    case Val::STR: return !v.s.empty();
+    case Val::TRUE_: return true;
+    default: return false;
+  }
+}
+
+int32_t intern_name(Cols& C, const std::string& s) {
+  auto it = C.intern.find(s);
+  if (it != C.intern.end()) return it->second;
+  const int32_t id = (int32_t)C.intern.size();
+  C.intern.emplace(s, id);
+  int64_t n = 0;
+  for (unsigned char c : s)
+    if ((c & 0xC0) != 0x80) ++n;
+  C.cp_total += n;
+  C.names += s;
+  C.name_off.push_back(C.cp_total);
+  return id;
+}
+
+template <size_t N>
+inline bool is(const std::pair<const char*, size_t>& k, const char (&w)[N]) {
+  return k.second == N - 1 && memcmp(k.first, w, N - 1) == 0;
+}
+
+// one record object; appends a row or drops it
+void record(Parser& P, Cols& C, bool strict) {
+  if (P.peek() != '{') throw Unsupported();  // non-object record: error path
+  ++P.p;
+  std::string scratch;
+  Val ph, cat, name, ts, dur;
+  bool has_args = false;
+  Val a[F_N];
+  bool args_other = false;
+  if (P.peek() == '}') {
+    ++P.p;
+  } else {
+    while (true) {
+      const auto key = P.key(scratch);
+      P.expect(':');
+      if (is(key, "ph")) ph = scalar(P);
+      else if (is(key, "cat")) cat = scalar(P);
+      else if (is(key, "name")) name = scalar(P);
+      else if (is(key, "ts")) ts = scalar(P);
+      else if (is(key, "dur")) dur = scalar(P);
+      else if (is(key, "args")) {
+        for (auto& x : a) x = Val();
+        args_other = false;
+        has_args = true;
+        if (P.peek() == '{') {
+          ++P.p;
+          if (P.peek() == '}') {
+            ++P.p;
+          } else {
+            while (true) {
+              const auto k = P.key(scratch);
+              P.expect(':');
+              int f = -1;
+              if (is(k, "Python id")) f = F_PID;
+              else if (is(k, "Python parent id")) f = F_PAR;
+              else if (is(k, "Sequence number")) f = F_SEQ;
+              else if (is(k, "Addr")) f = F_ADDR;
+              else if (is(k, "Bytes")) f = F_BYTES;
+              else if (is(k, "Total Allocated")) f = F_TA;
+              else if (is(k, "Total Reserved")) f = F_TR;
+              if (f >= 0) a[f] = scalar(P);
+              else P.skip();
+              const char d = P.peek();
+              ++P.p;
+              if (d == '}') break;
+              if (d != ',') throw Unsupported();
+            }
+          }
+        } else {
+          const Val v = scalar(P);  // `args or {}`: falsy -> {}
+          if (truthy(v) || v.t == Val::OTHER) args_other = true;
+        }
+      } else {
+        P.skip();
+      }
+      const char d = P.peek();
+      ++P.p;
+      if (d == '}') break;
+      if (d != ',') throw Unsupported();
+    }
+  }
+  (void)has_args;
+  if (ph.t == Val::STR && ph.s == "M") return;  // metadata record
+  int category = C_OTHER;
+  if (cat.t == Val::OTHER) throw Unsupported();  // unhashable: TypeError
+  if (cat.t == Val::STR) {
+    if (cat.s == "python_function") category = C_PF;
+    else if (cat.s == "cpu_op") category = C_OP;
+    else if (cat.s == "user_annotation") category = C_UA;
+    else if (cat.s == "cpu_instant_event") category = C_IN;
+    else if (cat.s != "other" && strict) throw Unsupported();
+  } else if (strict) {
+    throw Unsupported();
+  }
+  std::string nm;
+  if (name.t == Val::STR) nm = name.s;
+  else if (name.t != Val::ABSENT) throw Unsupported();  // str(non-string)
+  if (ts.t != Val::INT && ts.t != Val::FLT) throw Unsupported();  // incl. missing
+  double d = 0.0;
+  if (dur.t == Val::INT || dur.t == Val::FLT) d = dur.f;
+  else if (dur.t == Val::STR || dur.t == Val::OTHER) throw Unsupported();
+  else if (dur.t == Val::TRUE_) d = 1.0;
+  if (args_other && category != C_OTHER) throw Unsupported();
+  int64_t out[F_N];
+  for (int f = 0; f < F_N; ++f) out[f] = kNone;
+  if (category == C_PF) {
+    out[F_PID] = as_int(a[F_PID]);
+    out[F_PAR] = as_int(a[F_PAR]);
+  } else if (category == C_OP) {
+    const int64_t s = as_int(a[F_SEQ]);
+    out[F_SEQ] = (s != kNone && s < 0) ? kNone : s;
+  } else if (category == C_IN) {
+    const int64_t ad = as_int(a[F_ADDR]), nb = as_int(a[F_BYTES]);
+    if (ad == kNone || nb == kNone || nb == 0) {
+      if (strict) throw Unsupported();
+      C.dropped += 1;
+      return;
+    }
+    out[F_ADDR] = ad;
+    out[F_BYTES] = nb;
+    out[F_TA] = as_int(a[F_TA]);
+    out[F_TR] = as_int(a[F_TR]);
+  }
+  C.ts.push_back(ts.f);
+  C.dur.push_back(d);
+  C.cat.push_back((int8_t)category);
+  for (int f = 0; f < F_N; ++f) C.ints[f].push_back(out[f]);
+  C.name_id.push_back(intern_name(C, nm));
+}
+
+// ---- SHA-256 --------------------------------------------------------------------
+
+// OpenSSL's EVP SHA-256 (SHA-NI where the CPU has it, as Python's hashlib)
+struct Sha256 {
+  EVP_MD_CTX* ctx;
+  Sha256() : ctx(EVP_MD_CTX_new()) { EVP_DigestInit_ex(ctx, EVP_sha256(), nullptr); }
+  ~Sha256() { EVP_MD_CTX_free(ctx); }
+  void update(const void* p, size_t n) { EVP_DigestUpdate(ctx, p, n); }
+  void hex(char* out) {
+    unsigned char d[32];
+    unsigned int len = 0;
+    EVP_DigestFinal_ex(ctx, d, &len);
+    static const char* hx = "0123456789abcdef";
+    for (int i = 0; i < 32; ++i) {
+      out[2 * i] = hx[d[i] >> 4];
+      out[2 * i + 1] = hx[d[i] & 15];
+    }
+    out[64] = 0;
+  }
+};
+
+// streaming writer: buffered into the hash
+// json.dumps string with ensure_ascii=True (py_encode_basestring_ascii)
+void escape_json(std::string& b, const char* p, size_t n) {
+  b += '"';
+  size_t i = 0;
+  while (i < n) {
+    unsigned char c = (unsigned char)p[i];
+    uint32_t cp;
+    int len;
+    if (c < 0x80) { cp = c; len = 1; }
+    else if ((c >> 5) == 6) { cp = c & 0x1F; len = 2; }
+    else if ((c >> 4) == 14) { cp = c & 0x0F; len = 3; }
+    else { cp = c & 0x07; len = 4; }
+    for (int k = 1; k < len && i + k < n; ++k) cp = (cp << 6) | (p[i + k] & 0x3F);
+    i += len;
+    switch (cp) {
+      case '"': b += "\\\""; continue;
+      case '\\': b += "\\\\"; continue;
+      case '\n': b += "\\n"; continue;
+      case '\r': b += "\\r"; continue;
+      case '\t': b += "\\t"; continue;
+      case '\b': b += "\\b"; continue;
+      case '\f': b += "\\f"; continue;
+      default: break;
+    }
+    if (cp >= 0x20 && cp <= 0x7E) {
+      b += (char)cp;
+    } else if (cp < 0x10000) {
+      char t[8];
+      snprintf(t, sizeof t, "\\u%04x", cp);
+      b += t;
+    } else {
+      const uint32_t v = cp - 0x10000;
+      char t[16];
+      snprintf(t, sizeof t, "\\u%04x\\u%04x", 0xD800 | (v >> 10), 0xDC00 | (v & 0x3FF));
+      b += t;
+    }
+  }
+  b += '"';
+}
+
+struct Out {
+  Sha256 sh;
+  std::string b;
+  void s(const char* x) { b += x; flush_maybe(); }
+  void s(const std::string& x) { b += x; flush_maybe(); }
+  void c(char x) { b += x; }
+  void i(int64_t v) {
+    char t[24];
+    const auto r = std::to_chars(t, t + sizeof t, v);
+    b.append(t, r.ptr - t);
+  }
+  void flush_maybe() {
+    if (b.size() > (1u << 16)) {
+      sh.update(b.data(), b.size());
+      b.clear();
+    }
+  }
+  void str(const char* p, size_t n) {
+    escape_json(b, p, n);
+    flush_maybe();
+  }
+  void ilist(const int64_t* v, int64_t n) {
+    c('[');
+    for (int64_t k = 0; k < n; ++k) {
+      if (k) c(',');
+      i(v[k]);
+    }
+    c(']');
+  }
+  void done(char* hexout) {
+    sh.update(b.data(), b.size());
+    b.clear();
+    sh.hex(hexout);
+  }
+};
+
+}  // namespace
+
+extern "C" {
+
+const char* pm_ingest_last_error(void) { return g_err.c_str(); }
+
+// Parse; *handle receives an opaque column set (pm_ingest_free).  Returns 0,
+// PM_INGEST_UNSUPPORTED (5: use the Python reader) or PM_INGEST_EMPTY (7).
+int pm_ingest_json(const char* text, int64_t len, int strict, void** handle) {
+  *handle = nullptr;
+  Cols* C = new Cols();
+  C->name_off.push_back(0);
+  Parser P{text, text + len};
+  try {
+    const char c = P.peek();
+    if (c == '{') {
+      ++P.p;
+      bool found = false;
+      if (P.peek() != '}') {
+        while (true) {
+          const std::string key = P.str();
+          P.expect(':');
+          if (key == "traceEvents") {
+            if (found) throw Unsupported();  // duplicate key: last wins, rare
+            found = true;
+            P.expect('[');
+            if (P.peek() == ']') {
+              ++P.p;
+            } else {
+              while (true) {
+                record(P, *C, strict != 0);
+                const char d = P.peek();
+                ++P.p;
+                if (d == ']') break;
+                if (d != ',') throw Unsupported();
+              }
+            }
+          } else {
+            P.skip();
+          }
+          const char d = P.peek();
+          ++P.p;
+          if (d == '}') break;
+          if (d != ',') throw Unsupported();
+        }
+      } else {
+        ++P.p;
+      }
+      if (!found) throw Unsupported();
+    } else if (c == '[') {
+      ++P.p;
+      if (P.peek() == ']') {
+        ++P.p;
+      } else {
+        while (true) {
+          record(P, *C, strict != 0);
+          const char d = P.peek();
+          ++P.p;
+          if (d == ']') break;
+          if (d != ',') throw Unsupported();
+        }
+      }
+    } else {
+      throw Unsupported();
+    }
+    P.ws();
+    if (P.p != P.end) throw Unsupported();
+  } catch (const Unsupported&) {
+    delete C;
+    g_err = "outside the native reader's subset";
+    return PM_INGEST_UNSUPPORTED;
+  }
+  if (C->ts.empty()) {
+    delete C;
+    return PM_INGEST_EMPTY;
+  }
+  *handle = C;
+  return PM_INGEST_OK;
+}
+
+int64_t pm_ingest_count(void* h) { return (int64_t)static_cast<Cols*>(h)->ts.size(); }
+int64_t pm_ingest_dropped(void* h) { return static_cast<Cols*>(h)->dropped; }
+int64_t pm_ingest_n_names(void* h) { return (int64_t)static_cast<Cols*>(h)->intern.size(); }
+int64_t pm_ingest_names_bytes(void* h) { return (int64_t)static_cast<Cols*>(h)->names.size(); }
+
+// Copy the columns out: ints is F_N x n (field-major: python id, parent id,
+// sequence number, addr, bytes, total allocated, total reserved); name_id
+// (n) indexes the distinct-name table (name_off: n_names+1 code points).
+void pm_ingest_columns(void* h, double* ts, double* dur, int8_t* cat,
+                       int64_t* ints, int32_t* name_id, int64_t* name_off,
+                       char* names) {
+  Cols* C = static_cast<Cols*>(h);
+  const size_t n = C->ts.size();
+  memcpy(ts, C->ts.data(), n * sizeof(double));
+  memcpy(dur, C->dur.data(), n * sizeof(double));
+  memcpy(cat, C->cat.data(), n);
+  for (int f = 0; f < F_N; ++f) memcpy(ints + f * n, C->ints[f].data(), n * sizeof(int64_t));
+  memcpy(name_id, C->name_id.data(), n * sizeof(int32_t));
+  memcpy(name_off, C->name_off.data(), C->name_off.size() * sizeof(int64_t));
+  memcpy(names, C->names.data(), C->names.size());
+}
+
+void pm_ingest_free(void* h) { delete static_cast<Cols*>(h); }
+
+// SHA-256 of the estimator payload (estimator.py:189-202) from columns in
+// event-id order.  name_id (n) indexes a table of n_names names: UTF-8
+// blob + BYTE offsets (n_names+1).  ints as in
+// pm_ingest_columns.  sidecar_present 0 -> "sidecar": null.  max_split < 0
+// -> null.  Writes 64 hex chars + NUL to hex_out.
+int pm_bundle_digest(int64_t n, const int8_t* cat, const int64_t* start,
+                     const int64_t* dur, const int64_t* ints,
+                     const int32_t* name_id, int64_t n_names,
+                     const char* names, const int64_t* name_off,
+                     int sidecar_present, const int64_t* param_sizes,
+                     int64_t n_param, const int64_t* batch_bytes,
+                     int64_t n_batch, const char* optimizer,
+                     int64_t opt_len, int64_t sc_capacity, int64_t sc_initial,
+                     int64_t iterations, int64_t device_capacity,
+                     int64_t initial_memory, int64_t max_split,
+                     char* hex_out) {
+  static const char* cats[5] = {"python_function", "cpu_op", "user_annotation",
+                                "cpu_instant_event", "other"};
+  // args keys in sort order and their field index
+  static const struct { const char* k; int f; } args[7] = {
+      {"Addr", F_ADDR}, {"Bytes", F_BYTES}, {"Python id", F_PID},
+      {"Python parent id", F_PAR}, {"Sequence number", F_SEQ},
+      {"Total Allocated", F_TA}, {"Total Reserved", F_TR}};
+  std::vector<std::string> esc((size_t)n_names);
+  for (int64_t k = 0; k < n_names; ++k)
+    escape_json(esc[k], names + name_off[k], (size_t)(name_off[k + 1] - name_off[k]));
+  Out o;
+  o.s("{\"device_capacity\":");
+  o.i(device_capacity);
+  o.s(",\"initial_memory\":");
+  o.i(initial_memory);
+  o.s(",\"iterations\":");
+  o.i(iterations);
+  o.s(",\"max_split_size\":");
+  if (max_split < 0) o.s("null");
+  else o.i(max_split);
+  o.s(",\"sidecar\":");
+  if (!sidecar_present) {
+    o.s("null");
+  } else {
+    o.s("{\"batch_bytes\":");
+    o.ilist(batch_bytes, n_batch);
+    o.s(",\"device_capacity_bytes\":");
+    o.i(sc_capacity);
+    o.s(",\"initial_memory_bytes\":");
+    o.i(sc_initial);
+    o.s(",\"optimizer\":");
+    o.str(optimizer, (size_t)opt_len);
+    o.s(",\"param_sizes\":");
+    o.ilist(param_sizes, n_param);
+    o.c('}');
+  }
+  o.s(",\"trace\":{\"traceEvents\":[");
+  for (int64_t e = 0; e < n; ++e) {
+    if (e) o.c(',');
+    o.s("{\"args\":{");
+    bool first = true;
+    for (int k = 0; k < 7; ++k) {
+      const int64_t v = ints[args[k].f * n + e];
+      if (v == kNone) continue;
+      if (!first) o.c(',');
+      first = false;
+      o.c('"');
+      o.s(args[k].k);
+      o.s("\":");
+      o.i(v);
+    }
+    o.s("},\"cat\":\"");
+    o.s(cats[cat[e] < 0 || cat[e] > 4 ? 4 : cat[e]]);
+    o.s("\",\"dur\":");
+    o.i(dur[e]);
+    o.s(",\"name\":");
+    o.b += esc[name_id[e]];
+    o.s(cat[e] == C_IN ? ",\"ph\":\"i\",\"ts\":" : ",\"ph\":\"X\",\"ts\":");
+    o.i(start[e]);
+    o.c('}');
+    o.flush_maybe();
+  }
+  o.s("]}}");
+  o.done(hex_out);
+  return 0;
+}
+
+}  // extern "C"

@@ -17,7 +17,8 @@ from __future__ import annotations
 
 import numpy as np
 
-from .trace import CATEGORY_CODES, EventCategory, NONE, SidecarConfig, TraceBundle
+from .trace import (CATEGORY_CODES, EventCategory, NONE, NameColumn,
+                    SidecarConfig, TraceBundle)
 
 PF = CATEGORY_CODES[EventCategory.PYTHON_FUNCTION]
 OP = CATEGORY_CODES[EventCategory.CPU_OP]
@@ -138,7 +139,7 @@ def generate(leaves: int, iterations: int = 2, seed: int = 7,
                          optimizer_name="AdamW")
     return TraceBundle(category=cat[order], start=start[order] - start.min(),
                        duration=dur[order], ints=ints,
-                       names=_NameView(names, name_ids), metadata=side)
+                       names=NameColumn(names, name_ids), metadata=side)
 
 
 def _patch_step(cols, flat_index, dur):
@@ -148,17 +149,3 @@ def _patch_step(cols, flat_index, dur):
             arr[flat_index - n] = dur
             return
         n += len(arr)
-
-
-class _NameView:
-    """names[i] without materialising one string per event."""
-
-    def __init__(self, table, ids):
-        self.table = table
-        self.ids = ids
-
-    def __getitem__(self, i):
-        return self.table[int(self.ids[i])]
-
-    def __len__(self):
-        return len(self.ids)

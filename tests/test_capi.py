@@ -23,8 +23,9 @@ PIPE_HEADER = REPO / "include" / "peakmem_pipeline.h"
 
 def header_functions(header=HEADER):
     text = header.read_text()
-    return sorted(set(re.findall(r"^\s*(?:int|const char\*)\s+(pm_\w+)\(",
-                                 text, re.M)))
+    return sorted(set(re.findall(
+        r"^\s*(?:int|int64_t|void|const char\*)\s+(pm_\w+)\(",
+        text, re.M)))
 
 
 def test_header_declares_what_python_binds():
@@ -134,3 +135,18 @@ def test_engine_refuses_without_gpu(monkeypatch):
     from paper_2504_03887_b200.errors import EngineUnavailable
     with pytest.raises(EngineUnavailable):
         replay([{"seq_no": 0, "kind": "alloc", "block_id": 1, "size": 512}])
+
+
+def test_ingest_library_exports_every_declared_symbol():
+    from paper_2504_03887_b200 import _ingest
+    header = REPO / "include" / "peakmem_ingest.h"
+    assert header_functions(header) == sorted(_ingest.EXPORTED_SYMBOLS)
+    if not _ingest.LIB_PATH.exists():
+        import __graft_entry__
+        __graft_entry__.build()
+    out = subprocess.run(["nm", "-D", "--defined-only", str(_ingest.LIB_PATH)],
+                         capture_output=True, text=True, check=True).stdout
+    exported = set(re.findall(r"\bT (pm_\w+)", out))
+    for sym in header_functions(header):
+        assert sym in exported, sym
+    _ingest.load()
