@@ -136,6 +136,39 @@ int pm_replay_host(const pm_req_t* reqs, const int64_t* trace_offsets,
                    const int32_t* cfg_of_trace, pm_result_t* results,
                    int64_t* timeline, void* stream);
 
+/* ---- batched capacity bisection ------------------------
+ * The smallest device_capacity each trace replays in without OutOfMemory,
+ * found by bisection over whole-batch replays.  No reference function does
+ * the search; each probe is the reference's replay() with
+ * AllocatorConfig(device_capacity=C) (allocator.py:358-393), and the capacity
+ * enters only through `reserved + seg > cap` (allocator.py:258-287,
+ * 328-333), so the answer is a multiple of u = gcd(k_small_buffer,
+ * k_large_buffer, k_round_large).  Bracket: the unbounded peak_reserved
+ * runs; 0 OOMs, and with max_split_size None so does every C below the
+ * unbounded peak_allocated.  Bisection returns
+ * the C (multiple of u) that runs while C - u OOMs; if the allocator is not
+ * monotone in C a smaller runnable capacity may exist below an OOMing one.
+ *
+ * Device pointers; device_capacity in cfgs is ignored.  min_capacity[t]:
+ * the answer, 0 for a trace without allocations, -1 when the unbounded run
+ * is malformed (see unbounded[t].status).  n_probes[t]: bisection replays of
+ * trace t.  unbounded (nullable): round-0 results (peak_reserved = the
+ * reference's estimate).  probe_capacity / probe_results (nullable,
+ * [max_probes][n_traces]): the capacity and result of probe k of trace t.
+ * Synchronises `stream` once per round (to size the next round). */
+int pm_capacity_workspace_bytes(int64_t total_events, int64_t max_trace_events,
+                                int32_t n_traces, size_t* out_bytes);
+
+int pm_capacity_search(const pm_req_t* reqs, const int64_t* trace_offsets,
+                       int32_t n_traces, const pm_cfg_t* cfgs,
+                       const int32_t* cfg_of_trace, const int32_t* trace_order,
+                       int64_t* min_capacity, int32_t* n_probes,
+                       pm_result_t* unbounded, int64_t* probe_capacity,
+                       pm_result_t* probe_results, int32_t max_probes,
+                       void* workspace, size_t workspace_bytes,
+                       int64_t total_events, int64_t max_trace_events,
+                       void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -42,7 +42,8 @@ KIND_ALLOC, KIND_FREE, KIND_UNKNOWN, KIND_MISSING = 0, 1, 2, 3
 
 #: every symbol include/peakmem_b200.h declares
 EXPORTED_SYMBOLS = ("pm_last_error", "pm_version", "pm_replay_workspace_bytes",
-                    "pm_replay_batch", "pm_replay_host")
+                    "pm_replay_batch", "pm_replay_host",
+                    "pm_capacity_workspace_bytes", "pm_capacity_search")
 
 _lib = None
 
@@ -77,6 +78,13 @@ def load_library(path: Path | str | None = None) -> ctypes.CDLL:
                                     ctypes.c_size_t, i64, i64, vp]
     lib.pm_replay_host.restype = ctypes.c_int
     lib.pm_replay_host.argtypes = [vp, vp, i32, vp, i32, vp, vp, vp, vp]
+    lib.pm_capacity_workspace_bytes.restype = ctypes.c_int
+    lib.pm_capacity_workspace_bytes.argtypes = [
+        i64, i64, i32, ctypes.POINTER(ctypes.c_size_t)]
+    lib.pm_capacity_search.restype = ctypes.c_int
+    lib.pm_capacity_search.argtypes = [vp, vp, i32, vp, vp, vp, vp, vp, vp, vp,
+                                       vp, i32, vp, ctypes.c_size_t, i64, i64,
+                                       vp]
     if path is None:
         _lib = lib
     return lib

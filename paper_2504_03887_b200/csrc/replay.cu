@@ -33,12 +33,13 @@ constexpr int kWarps = 12;
 constexpr size_t kBucket_host = 32;  // warps (traces in flight) per CTA, 1 CTA / SM
 constexpr int kRetryWarps = 1;
 constexpr int kMaxRetryWarps = 64;
+constexpr long long kMaxMainWarps = 4096;  // >= SMs x warps per CTA
 
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 // workspace = ctl | retry list | retry pools | record table
 struct Layout {
-  size_t retry_list, gpool, recs, total;
+  size_t retry_list, hpool, gpool, recs, total;
   int nbmax_g;
   int retry_warps;
 };
@@ -50,6 +51,14 @@ Layout layout_for(int64_t total_events, int64_t max_trace_events,
   L.retry_list = off;
   off = align_up(off + 3 * sizeof(int32_t) * (size_t)(n_traces > 0 ? n_traces : 1),
                  256);
+  // main-kernel private overflow pools: one per resident warp (<= one per
+  // trace, and at most kMaxMainWarps)
+  {
+    long long w = ((long long)(n_traces > 0 ? n_traces : 1) + 15) / 16 * 16;
+    if (w > kMaxMainWarps) w = kMaxMainWarps;
+    L.hpool = off;
+    off = align_up(off + (size_t)w * pmb::kHpoolWarpBytes, 256);
+  }
   const int64_t mx = max_trace_events > 0 ? max_trace_events : 1;
   L.nbmax_g = (int)(mx / 8 + 4);
   int warps = n_traces < kMaxRetryWarps ? n_traces : kMaxRetryWarps;
@@ -66,13 +75,10 @@ Layout layout_for(int64_t total_events, int64_t max_trace_events,
 struct Occupancy {
   int sms = 0, per_sm = 0, buckets = 0, warps = 0;
   size_t smem = 0;
-  int per_sm1 = 0;  // tier-1 retry kernel
-  size_t smem1 = 0;
   int nbmax2 = 0;   // tier-2: one warp with a shared-memory directory
   size_t smem2 = 0;
 };
 
-constexpr int kTier1Warps = 8;  // tier 1: a dedicated 32-bucket pool per warp
 
 template <int W>
 int setup_kernel(int optin, int cap, int* buckets, size_t* smem, int* per_sm) {
@@ -94,7 +100,8 @@ int setup_kernel(int optin, int cap, int* buckets, size_t* smem, int* per_sm) {
 
 // Main pass: one CTA of `warps` warps per SM sharing a bucket pool sized to
 // the remaining shared memory (PM_POOL_BUCKETS caps it, PM_REPLAY_WARPS picks
-// 12 or 16 warps; 12 measured faster on C3).  Tier 1: 8 warps x 32 dedicated buckets.
+// 12 or 16 warps).  A trace the shared pool cannot hold is re-run by its warp
+// over a private 32-bucket HBM pool (kHpoolWarpBytes).
 int query_occupancy(Occupancy* out) {
   static std::mutex mu;
   static int cached_dev = -1;
@@ -122,10 +129,6 @@ int query_occupancy(Occupancy* out) {
       o.warps = 16;
       rc = setup_kernel<16>(optin, cap, &o.buckets, &o.smem, &o.per_sm);
     }
-    if (rc != PM_SUCCESS) return rc;
-    int b1 = 0;
-    rc = setup_kernel<kTier1Warps>(optin, kTier1Warps * 32, &b1, &o.smem1,
-                                   &o.per_sm1);
     if (rc != PM_SUCCESS) return rc;
     o.nbmax2 = (int)(((size_t)optin - 1024) / (kBucket_host * 24 + 32));
     while (o.nbmax2 > 8 && pmb::gmem_warp_bytes(o.nbmax2) > (size_t)optin) --o.nbmax2;
@@ -225,7 +228,6 @@ int replay_batch_impl(const pm_req_t* reqs, const int64_t* trace_offsets,
 
   cudaError_t e = cudaMemsetAsync(ctl, 0, sizeof(pmb::Ctl), stream);
   if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync");
-  int32_t* list1 = retry_list;
   int32_t* list2 = retry_list + n_traces;
   long long want = ((long long)n_traces + occ.warps - 1) / occ.warps;
   long long grid = (long long)occ.per_sm * occ.sms;
@@ -234,10 +236,16 @@ int replay_batch_impl(const pm_req_t* reqs, const int64_t* trace_offsets,
     const long long g = atoll(cap);
     if (g > 0 && g < grid) grid = g;
   }
+  if (grid * occ.warps > kMaxMainWarps) grid = kMaxMainWarps / occ.warps;
+  char* hpool = base + L.hpool;
+  // main pass; a trace that overflows the shared pool is re-run at once by
+  // its warp over a private HBM pool, and only one needing > 32 buckets is
+  // queued (list2) for the memory-directory tiers
 #define PM_LAUNCH_MAIN(W)                                                     \
   pmb::replay_smem_kernel<W><<<(unsigned)grid, W * 32, occ.smem, stream>>>(  \
       reqs, trace_offsets, cfgs, cfg_of_trace, results, timeline, recs, ctl, \
-      0, trace_order, n_traces, list1, occ.buckets, group_end, n_groups, ready)
+      0, trace_order, n_traces, list2, occ.buckets, group_end, n_groups,      \
+      ready, hpool)
   if (occ.warps == 12)
     PM_LAUNCH_MAIN(12);
   else
@@ -245,17 +253,6 @@ int replay_batch_impl(const pm_req_t* reqs, const int64_t* trace_offsets,
 #undef PM_LAUNCH_MAIN
   e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "replay_smem_kernel launch");
-  // tier 1: dedicated 32-bucket pools (grid sized for the worst case; idle
-  // CTAs exit at once when nothing overflowed)
-  long long grid1 = (long long)occ.per_sm1 * occ.sms;
-  long long want1 = ((long long)n_traces + kTier1Warps - 1) / kTier1Warps;
-  if (want1 < grid1) grid1 = want1;
-  pmb::replay_smem_kernel<kTier1Warps>
-      <<<(unsigned)grid1, kTier1Warps * 32, occ.smem1, stream>>>(
-          reqs, trace_offsets, cfgs, cfg_of_trace, results, timeline, recs,
-          ctl, 1, list1, 0, list2, kTier1Warps * 32, nullptr, 0, nullptr);
-  e = cudaGetLastError();
-  if (e != cudaSuccess) return cuda_fail(e, "replay tier-1 launch");
   {
     int32_t* list3 = retry_list + 2 * (size_t)n_traces;
     long long grid2 = occ.sms;
@@ -452,3 +449,266 @@ done:
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Batched capacity bisection: the smallest device capacity
+// each trace runs in, by bisection over many replays of the whole batch.
+//
+// The capacity enters the reference only through `reserved + seg > cap`
+// (allocator.py:258-287, 328-333), and reserved / seg are sums of segment
+// sizes, all multiples of u = gcd(k_small_buffer, k_large_buffer,
+// k_round_large) (segment_size_for, allocator.py:86-92).  So a run at
+// capacity C equals the run at floor(C/u)*u and the answer is a multiple of
+// u.  Bracket: the unbounded peak_reserved runs (that run never exceeds
+// it); below, capacity 0 OOMs on the first allocation, and when every block
+// is splittable (max_split_size None) so does anything below the unbounded
+// peak_allocated (reserved >= allocated = the sum of rounded live sizes).
+// Each round replays only the traces still bracketing, each at its own
+// midpoint (one pm_cfg_t per trace), until hi - lo == u.
+
+namespace {
+
+__device__ __host__ inline int64_t gcd64(int64_t a, int64_t b) {
+  while (b) {
+    const int64_t t = a % b;
+    a = b;
+    b = t;
+  }
+  return a;
+}
+
+struct CapLayout {
+  size_t replay, tcfg, iota, lo, hi, unit, active, count, res, total;
+};
+
+CapLayout cap_layout_for(int64_t total_events, int64_t max_trace_events,
+                         int32_t n_traces) {
+  CapLayout C;
+  const size_t n = (size_t)(n_traces > 0 ? n_traces : 1);
+  size_t off = 0;
+  C.replay = off;
+  off = align_up(off + layout_for(total_events, max_trace_events, n_traces).total, 256);
+  C.tcfg = off;
+  off = align_up(off + sizeof(pm_cfg_t) * n, 256);
+  C.iota = off;
+  off = align_up(off + 4 * n, 256);
+  C.lo = off;
+  off = align_up(off + 8 * n, 256);
+  C.hi = off;
+  off = align_up(off + 8 * n, 256);
+  C.unit = off;
+  off = align_up(off + 8 * n, 256);
+  C.active = off;
+  off = align_up(off + 4 * n, 256);
+  C.count = off;
+  off = align_up(off + 8, 256);
+  C.res = off;
+  off = align_up(off + sizeof(pm_result_t) * n, 256);
+  C.total = off;
+  return C;
+}
+
+__global__ void cap_prepare_kernel(const pm_cfg_t* __restrict__ cfgs,
+                                   const int32_t* __restrict__ cfg_of,
+                                   int32_t n, pm_cfg_t* __restrict__ tcfg,
+                                   int32_t* __restrict__ iota,
+                                   int32_t* __restrict__ n_probes) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  pm_cfg_t c = cfgs[cfg_of ? cfg_of[t] : 0];
+  c.device_capacity = -1;  // round 0: unbounded
+  tcfg[t] = c;
+  iota[t] = t;
+  n_probes[t] = 0;
+}
+
+// after round 0: bracket each trace (lo OOMs, hi runs), in units of u
+__global__ void cap_bracket_kernel(const pm_result_t* __restrict__ r0,
+                                   const pm_cfg_t* __restrict__ tcfg, int32_t n,
+                                   int64_t* __restrict__ lo, int64_t* __restrict__ hi,
+                                   int64_t* __restrict__ unit,
+                                   int64_t* __restrict__ min_cap,
+                                   pm_result_t* __restrict__ unbounded) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  const pm_result_t r = r0[t];
+  if (unbounded) unbounded[t] = r;
+  const pm_cfg_t c = tcfg[t];
+  const int64_t u = gcd64(gcd64(c.k_small_buffer, c.k_large_buffer), c.k_round_large);
+  unit[t] = u;
+  if (r.status != PM_OK) {  // malformed: no capacity answer
+    lo[t] = hi[t] = 0;
+    min_cap[t] = -1;
+    return;
+  }
+  // with max_split_size None every block is split to its rounded size, so
+  // allocated bytes do not depend on the capacity and any C below the
+  // unbounded peak_allocated OOMs; an unsplit oversize block (max_split
+  // set) makes allocated capacity-dependent, so the bracket starts at 0
+  lo[t] = (c.max_split_size < 0 && r.peak_allocated > 0)
+              ? (r.peak_allocated - 1) / u : -1;
+  hi[t] = r.peak_reserved / u;
+  min_cap[t] = 0;  // pending: cap_finish_kernel writes hi * u
+}
+
+// one block: the traces still bracketing (in LPT order) get their midpoint
+__global__ void cap_select_kernel(const int32_t* __restrict__ order, int32_t n,
+                                  const int64_t* __restrict__ lo,
+                                  const int64_t* __restrict__ hi,
+                                  const int64_t* __restrict__ unit,
+                                  pm_cfg_t* __restrict__ tcfg,
+                                  int32_t* __restrict__ active,
+                                  int64_t* __restrict__ count) {
+  __shared__ int warp_sum[32];
+  __shared__ int base;
+  if (threadIdx.x == 0) base = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int start = 0; start < n; start += blockDim.x) {
+    const int i = start + threadIdx.x;
+    const int t = i < n ? (order ? order[i] : i) : -1;
+    const bool on = t >= 0 && hi[t] - lo[t] > 1;
+    if (on) tcfg[t].device_capacity = (lo[t] + (hi[t] - lo[t]) / 2) * unit[t];
+    const unsigned m = __ballot_sync(0xffffffffu, on);
+    if (lane == 0) warp_sum[w] = __popc(m);
+    __syncthreads();
+    int before = 0, total = 0;
+    for (int k = 0; k < (int)(blockDim.x >> 5); ++k) {
+      if (k < w) before += warp_sum[k];
+      total += warp_sum[k];
+    }
+    if (on) active[base + before + __popc(m & ((1u << lane) - 1))] = t;
+    __syncthreads();
+    if (threadIdx.x == 0) base += total;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *count = base;
+}
+
+__global__ void cap_update_kernel(const int32_t* __restrict__ active, int32_t m,
+                                  const pm_result_t* __restrict__ res,
+                                  const pm_cfg_t* __restrict__ tcfg,
+                                  const int64_t* __restrict__ unit,
+                                  int64_t* __restrict__ lo, int64_t* __restrict__ hi,
+                                  int64_t* __restrict__ min_cap,
+                                  int32_t* __restrict__ n_probes,
+                                  int64_t* __restrict__ probe_capacity,
+                                  pm_result_t* __restrict__ probe_results,
+                                  int32_t max_probes, int32_t n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  const int t = active[i];
+  const pm_result_t r = res[t];
+  const int64_t cap = tcfg[t].device_capacity;
+  const int k = n_probes[t]++;
+  if (k < max_probes) {
+    if (probe_capacity) probe_capacity[(size_t)k * n + t] = cap;
+    if (probe_results) probe_results[(size_t)k * n + t] = r;
+  }
+  if (r.status == PM_OOM) {
+    lo[t] = cap / unit[t];
+  } else if (r.status == PM_OK) {
+    hi[t] = cap / unit[t];
+  } else {  // cannot happen after a clean unbounded run; stop the search
+    lo[t] = hi[t] - 1;
+    min_cap[t] = -2;
+  }
+}
+
+__global__ void cap_finish_kernel(int32_t n, const int64_t* __restrict__ hi,
+                                  const int64_t* __restrict__ unit,
+                                  int64_t* __restrict__ min_cap) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  if (min_cap[t] == 0) min_cap[t] = hi[t] * unit[t];
+}
+
+}  // namespace
+
+extern "C" {
+
+int pm_capacity_workspace_bytes(int64_t total_events, int64_t max_trace_events,
+                                int32_t n_traces, size_t* out_bytes) {
+  if (!out_bytes || total_events < 0 || max_trace_events < 0 || n_traces < 0)
+    return fail(PM_ERR_INVALID_ARGUMENT, "pm_capacity_workspace_bytes: bad args");
+  *out_bytes = cap_layout_for(total_events, max_trace_events, n_traces).total;
+  return PM_SUCCESS;
+}
+
+int pm_capacity_search(const pm_req_t* reqs, const int64_t* trace_offsets,
+                       int32_t n_traces, const pm_cfg_t* cfgs,
+                       const int32_t* cfg_of_trace, const int32_t* trace_order,
+                       int64_t* min_capacity, int32_t* n_probes,
+                       pm_result_t* unbounded, int64_t* probe_capacity,
+                       pm_result_t* probe_results, int32_t max_probes,
+                       void* workspace, size_t workspace_bytes,
+                       int64_t total_events, int64_t max_trace_events,
+                       void* stream_) {
+  if (n_traces < 0 || max_probes < 0)
+    return fail(PM_ERR_INVALID_ARGUMENT, "pm_capacity_search: negative size");
+  if (n_traces == 0) return PM_SUCCESS;
+  if (!min_capacity || !n_probes || !cfgs || !workspace)
+    return fail(PM_ERR_INVALID_ARGUMENT, "pm_capacity_search: null argument");
+  const CapLayout C = cap_layout_for(total_events, max_trace_events, n_traces);
+  if (workspace_bytes < C.total)
+    return fail(PM_ERR_WORKSPACE_TOO_SMALL,
+                "pm_capacity_search: workspace smaller than "
+                "pm_capacity_workspace_bytes()");
+  cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
+  char* base = static_cast<char*>(workspace);
+  void* rws = base + C.replay;
+  const size_t rws_bytes = C.tcfg - C.replay;
+  pm_cfg_t* tcfg = reinterpret_cast<pm_cfg_t*>(base + C.tcfg);
+  int32_t* iota = reinterpret_cast<int32_t*>(base + C.iota);
+  int64_t* lo = reinterpret_cast<int64_t*>(base + C.lo);
+  int64_t* hi = reinterpret_cast<int64_t*>(base + C.hi);
+  int64_t* unit = reinterpret_cast<int64_t*>(base + C.unit);
+  int32_t* active = reinterpret_cast<int32_t*>(base + C.active);
+  int64_t* count = reinterpret_cast<int64_t*>(base + C.count);
+  pm_result_t* res = reinterpret_cast<pm_result_t*>(base + C.res);
+  const unsigned blocks = (unsigned)((n_traces + 255) / 256);
+
+  cap_prepare_kernel<<<blocks, 256, 0, stream>>>(cfgs, cfg_of_trace, n_traces,
+                                                  tcfg, iota, n_probes);
+  int rc = replay_batch_impl(reqs, trace_offsets, n_traces, tcfg, iota,
+                             trace_order, res, nullptr, rws, rws_bytes,
+                             total_events, max_trace_events, stream_, nullptr,
+                             0, nullptr);
+  if (rc != PM_SUCCESS) return rc;
+  cap_bracket_kernel<<<blocks, 256, 0, stream>>>(res, tcfg, n_traces, lo, hi,
+                                                  unit, min_capacity, unbounded);
+  int64_t* h_count = nullptr;
+  cudaError_t e = cudaMallocHost((void**)&h_count, sizeof(int64_t));
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMallocHost");
+  for (int round = 0; round < 64; ++round) {
+    cap_select_kernel<<<1, 1024, 0, stream>>>(trace_order, n_traces, lo, hi,
+                                              unit, tcfg, active, count);
+    e = cudaMemcpyAsync(h_count, count, sizeof(int64_t), cudaMemcpyDeviceToHost,
+                        stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+    if (e != cudaSuccess) {
+      cudaFreeHost(h_count);
+      return cuda_fail(e, "pm_capacity_search: round sync");
+    }
+    const int32_t m = (int32_t)*h_count;
+    if (m == 0) break;
+    rc = replay_batch_impl(reqs, trace_offsets, m, tcfg, iota, active, res,
+                           nullptr, rws, rws_bytes, total_events,
+                           max_trace_events, stream_, nullptr, 0, nullptr);
+    if (rc != PM_SUCCESS) {
+      cudaFreeHost(h_count);
+      return rc;
+    }
+    cap_update_kernel<<<(unsigned)((m + 255) / 256), 256, 0, stream>>>(
+        active, m, res, tcfg, unit, lo, hi, min_capacity, n_probes,
+        probe_capacity, probe_results, max_probes, n_traces);
+  }
+  cudaFreeHost(h_count);
+  cap_finish_kernel<<<blocks, 256, 0, stream>>>(n_traces, hi, unit, min_capacity);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "pm_capacity_search launch");
+  return PM_SUCCESS;
+}
+
+}  // extern "C"
+

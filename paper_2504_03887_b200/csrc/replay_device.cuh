@@ -1034,7 +1034,8 @@ __device__ __forceinline__ void replay_trace(
 
 struct Ctl {
   unsigned work[4];   // work counters: main pass, tiers 1, 2 and 3
-  unsigned n_list[4]; // traces queued for tier 1 / 2 / 3 (index 1..3)
+  unsigned n_list[4]; // [1]: in-warp HBM re-runs (count); [2], [3]: traces
+                      // queued for the tier-2 / tier-3 kernels
   unsigned pad[56];
 };
 
@@ -1051,6 +1052,10 @@ __host__ __device__ __forceinline__ size_t gmem_warp_bytes(int nbmax) {
   return ((size_t)nbmax * kBucket * 24 + 32 * 24 + (size_t)nbmax * 32 + 255) /
          256 * 256;
 }
+
+// Per-warp private overflow pool of the main kernel (HBM, L2-resident):
+// 32 buckets of entries plus the in-use word its DirReg allocates from.
+constexpr size_t kHpoolWarpBytes = (size_t)kBucket * kBucket * 24 + 256;
 
 __device__ __forceinline__ void carve_pool(char* base, int nbuckets, Pool& P) {
   const size_t E = (size_t)nbuckets * kBucket;
@@ -1083,7 +1088,8 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
                        int pass, const int32_t* __restrict__ list, int n_host,
                        int32_t* __restrict__ overflow_list, int buckets,
                        const unsigned* __restrict__ group_end, int n_groups,
-                       const volatile unsigned* ready) {
+                       const volatile unsigned* ready,
+                       char* __restrict__ hpool) {
   extern __shared__ __align__(16) char smem[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
@@ -1121,8 +1127,27 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
     replay_trace(tr, reqs, offs, cfgs, cfg_of, results, timeline, recs, P,
                  dir, kBucket, st, lane);
     __syncwarp();
-    if (lane == 0 && results[tr].status == PM_POOL_OVERFLOW) {
-      const unsigned k = atomicAdd(&ctl->n_list[pass + 1], 1u);
+    int sts = __shfl_sync(kFull, lane == 0 ? results[tr].status : 0, 0);
+    if (sts == PM_POOL_OVERFLOW && hpool != nullptr) {
+      // the CTA's shared pool ran dry (or the trace needs > 32 buckets):
+      // re-run at once in this warp over its private 32-bucket HBM pool
+      if (lane == 0) atomicAdd(&ctl->n_list[1], 1u);  // diagnostic count
+      char* hb = hpool + ((size_t)blockIdx.x * WARPS + wib) * kHpoolWarpBytes;
+      Pool HP;
+      carve_pool(hb, kBucket, HP);
+      DirReg hdir;
+      hdir.cta_used = reinterpret_cast<unsigned*>(hb + (size_t)kBucket * kBucket * 24);
+      hdir.cta_words = 1;
+      hdir.cta_buckets = kBucket;
+      if (lane == 0) *hdir.cta_used = 0u;
+      __syncwarp();
+      replay_trace(tr, reqs, offs, cfgs, cfg_of, results, timeline, recs, HP,
+                   hdir, kBucket, st, lane);
+      __syncwarp();
+      sts = __shfl_sync(kFull, lane == 0 ? results[tr].status : 0, 0);
+    }
+    if (lane == 0 && sts == PM_POOL_OVERFLOW) {
+      const unsigned k = atomicAdd(&ctl->n_list[2], 1u);  // tier-2 queue
       overflow_list[k] = tr;
     }
   }

@@ -86,3 +86,41 @@ class DeviceBatch:
     def timeline(self) -> np.ndarray:
         self.torch.cuda.synchronize(self.device)
         return self.d_timeline.cpu().numpy().view(np.int64).copy()
+
+    def capacity_search(self, max_probes: int = 64, stream=None) -> dict:
+        """Bisect every trace's smallest runnable device capacity
+        (pm_capacity_search; synchronises once per bisection round).
+
+        Returns numpy arrays: min_capacity (n), n_probes (n), unbounded
+        (n results), probe_capacity / probe_results ([max_probes, n])."""
+        torch = self.torch
+        lib = self.lib
+        n = self.n_traces
+        out = ctypes.c_size_t(0)
+        _native.check(lib.pm_capacity_workspace_bytes(
+            self.total_events, self.max_trace_events, n, ctypes.byref(out)), lib)
+        ws = torch.empty(int(out.value), dtype=torch.uint8, device=self.device)
+        dev = self.device
+        d_min = torch.zeros(n, dtype=torch.int64, device=dev)
+        d_np = torch.zeros(n, dtype=torch.int32, device=dev)
+        d_unb = torch.zeros(n * RESULT_DTYPE.itemsize, dtype=torch.uint8, device=dev)
+        d_pcap = torch.full((max_probes * n,), -1, dtype=torch.int64, device=dev)
+        d_pres = torch.zeros(max_probes * n * RESULT_DTYPE.itemsize,
+                             dtype=torch.uint8, device=dev)
+        s = stream if stream is not None else torch.cuda.current_stream(dev)
+        _native.check(lib.pm_capacity_search(
+            self._ptr(self.d_reqs), self._ptr(self.d_offsets), n,
+            self._ptr(self.d_cfgs), self._ptr(self.d_cfg_of),
+            self._ptr(self.d_order), self._ptr(d_min), self._ptr(d_np),
+            self._ptr(d_unb), self._ptr(d_pcap), self._ptr(d_pres), max_probes,
+            self._ptr(ws), int(out.value), self.total_events,
+            self.max_trace_events, ctypes.c_void_p(s.cuda_stream)), lib)
+        torch.cuda.synchronize(dev)
+        return {
+            "min_capacity": d_min.cpu().numpy(),
+            "n_probes": d_np.cpu().numpy(),
+            "unbounded": d_unb.cpu().numpy().view(RESULT_DTYPE).copy(),
+            "probe_capacity": d_pcap.cpu().numpy().reshape(max_probes, n),
+            "probe_results": d_pres.cpu().numpy().view(RESULT_DTYPE)
+                                   .reshape(max_probes, n).copy(),
+        }

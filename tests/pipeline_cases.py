@@ -35,48 +35,60 @@ CASES = [
 ]
 
 
+def ev(cat, name, ts, dur=None, **args):
+    rec = {"ph": "i" if cat == "cpu_instant_event" else "X",
+           "cat": cat, "name": name, "ts": ts, "args": args}
+    if dur is not None:
+        rec["dur"] = dur
+    return rec
+
+
+def instant(ts, addr, nbytes):
+    return ev("cpu_instant_event", "[memory]", ts, Addr=addr, Bytes=nbytes)
+
+
+def iteration_records(k, base, with_grad_free_at=None, with_span_blocks=True):
+    """One iteration of the reference conftest's layout at `base`
+    (pkg/tests/conftest.py:50-89, restated): ProfilerStep [0, 900),
+    zero-grad at +10, a Linear forward at +60 with a retained 1000 B
+    activation and a 500 B intra-op temporary, an unowned 123 B block at
+    +150, backward at +200 with a 400 B gradient, an optimizer step
+    [+400, +500) with an optional surviving 400 B state block and two
+    span-local temporaries."""
+    pid, seq = 10 + k, 100 + k
+    recs = [
+        ev("user_annotation", f"ProfilerStep#{k}", base, 900),
+        ev("user_annotation", "Optimizer.zero_grad#SGD.zero_grad", base + 10, 20),
+        ev("python_function", "nn.Module: Linear_0", base + 50, 100,
+           **{"Python id": pid}),
+        ev("cpu_op", "aten::linear", base + 60, 50, **{"Sequence number": seq}),
+        instant(base + 70, 0x1000 + k, 1000),
+        instant(base + 72, 0x2000 + k, 500),
+        instant(base + 80, 0x2000 + k, -500),
+        instant(base + 150, 0x7000 + k, 123),
+        ev("cpu_op", "autograd::engine::evaluate_function: AddmmBackward0",
+           base + 200, 100, **{"Sequence number": seq}),
+        instant(base + 230, 0x1000 + k, -1000),
+        instant(base + 250, 0x3000 + k, 400),
+        ev("user_annotation", "Optimizer.step#SGD.step", base + 400, 100),
+        instant(base + 600, 0x7000 + k, -123),
+    ]
+    if with_span_blocks:
+        recs += [instant(base + 420, 0x4000 + k, 400),
+                 instant(base + 430, 0x5000 + k, 999),
+                 instant(base + 440, 0x5000 + k, -999),
+                 instant(base + 435, 0x6000 + k, 400),
+                 instant(base + 450, 0x6000 + k, -400)]
+    if with_grad_free_at is not None:
+        recs.append(instant(with_grad_free_at, 0x3000 + k, -400))
+    return recs
+
+
 def _conftest_records():
     """Two iterations of the reference conftest layout at base 0 and 1000,
     the first with a gradient free at +1010 (test_orchestration.py)."""
-    def ev(cat, name, ts, dur=None, **args):
-        rec = {"ph": "i" if cat == "cpu_instant_event" else "X",
-               "cat": cat, "name": name, "ts": ts, "args": args}
-        if dur is not None:
-            rec["dur"] = dur
-        return rec
-
-    def instant(ts, addr, nbytes):
-        return ev("cpu_instant_event", "[memory]", ts, Addr=addr, Bytes=nbytes)
-
-    def it(k, base, grad_free=None):
-        pid, seq = 10 + k, 100 + k
-        recs = [
-            ev("user_annotation", f"ProfilerStep#{k}", base, 900),
-            ev("user_annotation", "Optimizer.zero_grad#SGD.zero_grad", base + 10, 20),
-            ev("python_function", "nn.Module: Linear_0", base + 50, 100,
-               **{"Python id": pid}),
-            ev("cpu_op", "aten::linear", base + 60, 50, **{"Sequence number": seq}),
-            instant(base + 70, 0x1000 + k, 1000),
-            instant(base + 72, 0x2000 + k, 500),
-            instant(base + 80, 0x2000 + k, -500),
-            instant(base + 150, 0x7000 + k, 123),
-            ev("cpu_op", "autograd::engine::evaluate_function: AddmmBackward0",
-               base + 200, 100, **{"Sequence number": seq}),
-            instant(base + 230, 0x1000 + k, -1000),
-            instant(base + 250, 0x3000 + k, 400),
-            ev("user_annotation", "Optimizer.step#SGD.step", base + 400, 100),
-            instant(base + 600, 0x7000 + k, -123),
-            instant(base + 420, 0x4000 + k, 400),
-            instant(base + 430, 0x5000 + k, 999),
-            instant(base + 440, 0x5000 + k, -999),
-            instant(base + 435, 0x6000 + k, 400),
-            instant(base + 450, 0x6000 + k, -400),
-        ]
-        if grad_free is not None:
-            recs.append(instant(grad_free, 0x3000 + k, -400))
-        return recs
-
-    recs = it(0, 0, grad_free=1010) + it(1, 1000)
+    recs = (iteration_records(0, 0, with_grad_free_at=1010)
+            + iteration_records(1, 1000))
     side = {"param_sizes": [400], "batch_bytes": [128, 64], "optimizer": "sgd",
             "device_capacity_bytes": 0, "initial_memory_bytes": 0}
     return recs, side

@@ -23,6 +23,9 @@ def main():
     ap.add_argument("--leaves", type=int, nargs="+", default=[6000])
     ap.add_argument("--iterations", type=int, default=2)
     ap.add_argument("--check", action="store_true")
+    ap.add_argument("--file", action="store_true",
+                    help="also time the user path: write the trace as chrome "
+                         "JSON, then parse_trace + estimate from the file")
     args = ap.parse_args()
     import torch
     import __graft_entry__
@@ -61,6 +64,22 @@ def main():
             line["oracle_s"] = time.perf_counter() - tc
             line["oracle_equal"] = want == [(r.kind.value, r.block_id, r.size,
                                              r.virtual_ts) for r in seq.requests]
+        if args.file:
+            import tempfile
+            from paper_2504_03887_b200.trace import parse_trace
+            with tempfile.TemporaryDirectory() as d:
+                path = Path(d) / "c5.trace.json"
+                path.write_text(json.dumps(b.to_json_dict()))
+                line["file_mb"] = path.stat().st_size / 1e6
+                tf = time.perf_counter()
+                pb = parse_trace(path, b.metadata)
+                tg = time.perf_counter()
+                est = api.PeakMemoryEstimator(iterations=args.iterations)
+                rep = est.estimate(pb)
+                th = time.perf_counter()
+            line.update({"parse_s": tg - tf, "estimate_s": th - tg,
+                         "file_to_report_s": th - tf,
+                         "file_peak_equal": rep.reserved_peak == res.peak_reserved})
         print(json.dumps(line), flush=True)
 
 
