@@ -487,8 +487,7 @@ __device__ __forceinline__ bool split_bucket(const Pool& P, D& dir, int d,
                                              int hcmp, int lane) {
   // a full directory first merges an adjacent pair; the caller re-finds
   // its bucket and retries (the merge always frees a directory slot)
-  if (dir.full()) return try_merge(P, dir, rec, st, hcmp, lane);
-  const int q = dir.alloc_phys();
+  const int q = dir.full() ? -1 : dir.alloc_phys();
   if (q < 0) return try_merge(P, dir, rec, st, hcmp, lane);
   const int p = dir.phys(d);
   const int base = p * kBucket;
@@ -586,25 +585,27 @@ __device__ __forceinline__ int pool_remove(const Pool& P, D& dir, Ctx& c,
   return moved;
 }
 
-// New (key, addr) for entry `id` (links already set).  Returns its id after
-// the update (-1 on overflow); a moved entry has its neighbours re-pointed.
+// Rekey entry `id` to (k, a, links) -- in place when it stays in its bucket
+// -- or, with id < 0, insert a new entry.  Returns the entry's id (-1 on
+// overflow).  The caller re-points the entry's neighbours (relink).  The
+// single call site keeps one inlined copy of insert / split / merge.
 template <class D>
-__device__ __forceinline__ int pool_rekey(const Pool& P, D& dir, Ctx& c,
-                                          int id, u64 k, u64 a,
-                                          const Recs& rec, const Stage& st,
-                                          int hcmp, int lane) {
-  const int d = dir.find(k, a);
-  if (dir.phys(d) == id / kBucket) {
-    __syncwarp();
-    P.key[id] = k;
-    P.addr[id] = a;
-    return id;
+__device__ __forceinline__ int pool_upsert(const Pool& P, D& dir, Ctx& c,
+                                           int id, u64 k, u64 a, u64 links,
+                                           const Recs& rec, const Stage& st,
+                                           int hcmp, int lane) {
+  if (id >= 0) {
+    const int d = dir.find(k, a);
+    if (dir.phys(d) == id / kBucket) {
+      __syncwarp();
+      P.key[id] = k;
+      P.addr[id] = a;
+      P.links[id] = links;
+      return id;
+    }
+    pool_remove(P, dir, c, id, rec, st, hcmp, lane);
   }
-  const u64 links = P.links[id];
-  pool_remove(P, dir, c, id, rec, st, hcmp, lane);
-  const int nid = pool_insert(P, dir, c, k, a, links, rec, st, hcmp, lane);
-  if (nid >= 0) relink(rec, st, hcmp, lane, links, nid);
-  return nid;
+  return pool_insert(P, dir, c, k, a, links, rec, st, hcmp, lane);
 }
 
 // Best fit (allocator.py:203-221): argmin (key, addr) with
@@ -696,25 +697,24 @@ __device__ __forceinline__ void make_room(const Pool& P, D& dir, Ctx& c,
                                           const Recs& rec, const Stage& st,
                                           int hcmp, int lane) {
   const long long capacity = cf.cp->device_capacity;
-  if (cf.max_split >= 0) {
-    while (c.reserved + seg > capacity) {
-      const int id = find_release_candidate(P, dir, cf.max_split, lane);
-      if (id < 0) break;
-      const long long sz = (long long)(P.key[id] & kSizeMask);
-      pool_remove(P, dir, c, id, rec, st, hcmp, lane);
-      c.reserved -= sz;
-      c.nseg -= 1;
+  // stage 1 (max_split set): threshold max_split, stop once it fits;
+  // stage 2: threshold -1 (every wholly-free segment), entered only if it
+  // still does not fit, runs until no candidate is left
+  int stage = cf.max_split >= 0 ? 1 : 2;
+  if (stage == 2 && c.reserved + seg <= capacity) return;
+  for (;;) {
+    if (stage == 1 && c.reserved + seg <= capacity) break;
+    const int id = find_release_candidate(
+        P, dir, stage == 1 ? cf.max_split : -1, lane);
+    if (id < 0) {
+      if (stage == 2 || c.reserved + seg <= capacity) break;
+      stage = 2;
+      continue;
     }
-  }
-  if (c.reserved + seg > capacity) {
-    for (;;) {
-      const int id = find_release_candidate(P, dir, -1, lane);
-      if (id < 0) break;
-      const long long sz = (long long)(P.key[id] & kSizeMask);
-      pool_remove(P, dir, c, id, rec, st, hcmp, lane);
-      c.reserved -= sz;
-      c.nseg -= 1;
-    }
+    const long long sz = (long long)(P.key[id] & kSizeMask);
+    pool_remove(P, dir, c, id, rec, st, hcmp, lane);
+    c.reserved -= sz;
+    c.nseg -= 1;
   }
 }
 
@@ -792,105 +792,179 @@ __device__ __forceinline__ void replay_trace(
         sts = kind == PM_KIND_UNKNOWN ? PM_UNKNOWN_KIND : PM_MISSING_FIELD;
       } else if ((unsigned)hj >= (unsigned long long)n) {
         sts = PM_BAD_HANDLE;
-      } else if (kind == PM_KIND_ALLOC) {
-        // allocate (allocator.py:273-292): duplicate, then zero size
-        const unsigned strm = ks >> 2;
-        const u64 rounded = ((u64)size + amask) & ~amask;
-        if (st.k[src] != 0) {
-          sts = PM_DUPLICATE_HANDLE;
-        } else if (size <= 0) {
-          sts = PM_ZERO_SIZE;
-        } else if (strm > 0xFFFFu) {
-          sts = PM_BAD_STREAM;
-        } else if (rounded > kSizeMask) {
-          sts = PM_SIZE_LIMIT;
-        } else {
-          u64 out_a = 0, out_k = 0;
-          u32 out_L = kNone, out_R = kNone;
-          const u64 sbits = (u64)strm << kSizeBits;
-          const u64 lo = sbits | rounded;
-          u64 span = kSizeMask + 1 - rounded;
-          if (cf.max_split >= 0 && (u64)cf.max_split < span)
-            span = (u64)cf.max_split;
-          const int id = best_fit(P, dir, lo, span, lane);
-          if (id >= 0) {
-            // hit: _take (allocator.py:234-242), _split (:223-232)
-            const u64 K = P.key[id];
-            const u64 A = P.addr[id];
-            const u64 Lk = P.links[id];
-            const u32 Lf = lo32(Lk), Rf = hi32(Lk);
-            PM_UNIFORM(id);
-            PM_UNIFORM(Lk);
-            PM_UNIFORM(K);
-            PM_UNIFORM(A);
-            const u64 S = K & kSizeMask;
-            const bool splittable =
-                cf.max_split < 0 || (long long)S <= cf.max_split;
-            out_a = A;
-            out_L = Lf;
-            if (splittable && S > rounded) {
-              __syncwarp();
-              P.links[id] = mk_links((u32)hj, Rf);
-              const int tid = pool_rekey(P, dir, c, id, sbits | (S - rounded),
-                                         A + rounded, rec, st, hcmp, lane);
-              if (tid < 0) {
-                sts = PM_POOL_OVERFLOW;
-              } else {
+      } else {
+        // Plan the pool work of this request (warp-uniform), then run it at
+        // single sites: B) remove an entry, C) rekey-or-insert an entry and
+        // re-point its neighbours, D) up to two further link fixes.
+        int rm_id = -1;           // B
+        bool up = false;          // C
+        int up_id = -1;
+        u64 up_k = 0, up_a = 0, up_l = 0;
+        u32 f1 = kNone, f2 = kNone;  // D: (f1 right ref, f2 left ref) := hj
+        int both_pid = -1;        // free merging on both sides
+        u64 both_S = 0, both_rk = 0;
+        u32 both_rR = kNone;
+        bool is_alloc = kind == PM_KIND_ALLOC;
+        bool split_out = false;   // alloc: out_R is the remainder entry
+        u64 out_a = 0, out_k = 0;
+        u32 out_L = kNone, out_R = kNone;
+        if (is_alloc) {
+          // allocate (allocator.py:273-292): duplicate, then zero size
+          const unsigned strm = ks >> 2;
+          const u64 rounded = ((u64)size + amask) & ~amask;
+          if (st.k[src] != 0) {
+            sts = PM_DUPLICATE_HANDLE;
+          } else if (size <= 0) {
+            sts = PM_ZERO_SIZE;
+          } else if (strm > 0xFFFFu) {
+            sts = PM_BAD_STREAM;
+          } else if (rounded > kSizeMask) {
+            sts = PM_SIZE_LIMIT;
+          } else {
+            const u64 sbits = (u64)strm << kSizeBits;
+            const u64 lo = sbits | rounded;
+            u64 span = kSizeMask + 1 - rounded;
+            if (cf.max_split >= 0 && (u64)cf.max_split < span)
+              span = (u64)cf.max_split;
+            const int id = best_fit(P, dir, lo, span, lane);
+            if (id >= 0) {
+              // hit: _take (allocator.py:234-242), _split (:223-232)
+              const u64 K = P.key[id];
+              const u64 A = P.addr[id];
+              const u64 Lk = P.links[id];
+              const u32 Lf = lo32(Lk), Rf = hi32(Lk);
+              const u64 S = K & kSizeMask;
+              const bool splittable =
+                  cf.max_split < 0 || (long long)S <= cf.max_split;
+              out_a = A;
+              out_L = Lf;
+              f1 = Lf;
+              if (splittable && S > rounded) {
+                up = true;
+                up_id = id;
+                up_k = sbits | (S - rounded);
+                up_a = A + rounded;
+                up_l = mk_links((u32)hj, Rf);
                 out_k = sbits | rounded;
-                out_R = kFreeTag | (u32)tid;
+                split_out = true;
+              } else {
+                rm_id = id;
+                out_k = K;
+                out_R = Rf;
+                f2 = Rf;
               }
             } else {
-              pool_remove(P, dir, c, id, rec, st, hcmp, lane);
-              out_k = K;
-              out_R = Rf;
-              if (Rf != kNone) set_link(rec, st, hcmp, lane, Rf, 0, (u32)hj);
-            }
-            if (Lf != kNone) set_link(rec, st, hcmp, lane, Lf, 1, (u32)hj);
-          } else {
-            // miss: new segment (allocator.py:278-288, 244-250)
-            const long long seg = segment_size_for((long long)rounded, cf);
-            const long long capacity = cp->device_capacity;
-            if (capacity >= 0 && c.reserved + seg > capacity) {
-              make_room(P, dir, c, seg, cf, rec, st, hcmp, lane);
-              if (c.reserved + seg > capacity) sts = PM_OOM;
-            }
-            if (sts == PM_OK && (u64)seg > kSizeMask) sts = PM_SIZE_LIMIT;
-            if (sts == PM_OK) {
-              const u64 A = (u64)c.next_base;
-              c.next_base += seg;
-              c.reserved += seg;
-              c.nseg += 1;
-              c.nseg_peak = max(c.nseg_peak, c.nseg);
-              const bool splittable = cf.max_split < 0 || seg <= cf.max_split;
-              out_a = A;
-              if (splittable && (u64)seg > rounded) {
-                const int tid = pool_insert(
-                    P, dir, c, sbits | ((u64)seg - rounded), A + rounded,
-                    mk_links((u32)hj, kNone), rec, st, hcmp, lane);
-                if (tid < 0) {
-                  sts = PM_POOL_OVERFLOW;
-                } else {
+              // miss: new segment (allocator.py:278-288, 244-250)
+              const long long seg = segment_size_for((long long)rounded, cf);
+              const long long capacity = cp->device_capacity;
+              if (capacity >= 0 && c.reserved + seg > capacity) {
+                make_room(P, dir, c, seg, cf, rec, st, hcmp, lane);
+                if (c.reserved + seg > capacity) sts = PM_OOM;
+              }
+              if (sts == PM_OK && (u64)seg > kSizeMask) sts = PM_SIZE_LIMIT;
+              if (sts == PM_OK) {
+                const u64 A = (u64)c.next_base;
+                c.next_base += seg;
+                c.reserved += seg;
+                c.nseg += 1;
+                c.nseg_peak = max(c.nseg_peak, c.nseg);
+                const bool splittable = cf.max_split < 0 || seg <= cf.max_split;
+                out_a = A;
+                if (splittable && (u64)seg > rounded) {
+                  up = true;
+                  up_k = sbits | ((u64)seg - rounded);
+                  up_a = A + rounded;
+                  up_l = mk_links((u32)hj, kNone);
                   out_k = sbits | rounded;
-                  out_R = kFreeTag | (u32)tid;
+                  split_out = true;
+                } else {
+                  out_k = sbits | (u64)seg;
                 }
-              } else {
-                out_k = sbits | (u64)seg;
               }
             }
           }
-          PM_UNIFORM(out_L);
-          PM_UNIFORM(out_R);
-          PM_UNIFORM(out_k);
-          PM_UNIFORM(out_a);
-          PM_UNIFORM(sts);
+        } else {
+          // free (allocator.py:294-320): double free before unknown handle
+          const u64 rkj = st.k[src];
+          if (rkj == kFreed) {
+            sts = PM_DOUBLE_FREE;
+          } else if (rkj == 0) {
+            sts = PM_UNKNOWN_HANDLE;
+          } else {
+            const u64 A = st.a[src];
+            const u32 L = st.L[src], R = st.R[src];
+            const u64 S = rkj & kSizeMask;
+            c.allocated -= (long long)S;
+            const bool lf = is_free_ref(L), rf = is_free_ref(R);
+            up = true;
+            if (!lf && !rf) {
+              up_k = rkj;
+              up_a = A;
+              up_l = mk_links(L, R);
+            } else if (lf && !rf) {
+              // the free block on the left absorbs this one
+              const int pid = (int)(L & ~kFreeTag);
+              up_id = pid;
+              up_k = P.key[pid] + S;
+              up_a = P.addr[pid];
+              up_l = mk_links(lo32(P.links[pid]), R);
+            } else if (!lf && rf) {
+              // the free block on the right absorbs this one
+              const int rid = (int)(R & ~kFreeTag);
+              up_id = rid;
+              up_k = P.key[rid] + S;
+              up_a = A;
+              up_l = mk_links(L, hi32(P.links[rid]));
+            } else {
+              // left absorbs this block and the right free block: the
+              // right entry goes first (B), then the left is rekeyed (C)
+              const int rid = (int)(R & ~kFreeTag);
+              both_pid = (int)(L & ~kFreeTag);
+              both_rk = P.key[rid];
+              both_rR = hi32(P.links[rid]);
+              both_S = S;
+              rm_id = rid;
+            }
+          }
+        }
+        if (sts == PM_OK) {
+          if (rm_id >= 0) {  // B
+            const int moved = pool_remove(P, dir, c, rm_id, rec, st, hcmp, lane);
+            if (both_pid >= 0) {
+              const int pid = moved == both_pid ? rm_id : both_pid;
+              up_id = pid;
+              up_k = P.key[pid] + both_S + (both_rk & kSizeMask);
+              up_a = P.addr[pid];
+              up_l = mk_links(lo32(P.links[pid]), both_rR);
+            }
+          }
+          if (up) {  // C
+            const int nid = pool_upsert(P, dir, c, up_id, up_k, up_a, up_l,
+                                        rec, st, hcmp, lane);
+            if (nid < 0) {
+              sts = PM_POOL_OVERFLOW;
+            } else {
+              relink(rec, st, hcmp, lane, up_l, nid);
+              if (split_out) out_R = kFreeTag | (u32)nid;
+            }
+          }
+        }
+        if (sts == PM_OK) {
+          // D: the taken block's allocated neighbours now point at hj
+          if (f2 != kNone) set_link(rec, st, hcmp, lane, f2, 0, (u32)hj);
+          if (f1 != kNone) set_link(rec, st, hcmp, lane, f1, 1, (u32)hj);
           PM_UNIFORM(dir.nb);
           PM_UNIFORM(c.F);
-          if (sts == PM_OK) {
-            __syncwarp();  // order after any mirror / link store to hj
+          c.maxF = max(c.maxF, c.F);
+          __syncwarp();  // order after any mirror / link store to hj
+          if (is_alloc) {
+            PM_UNIFORM(out_L);
+            PM_UNIFORM(out_R);
+            PM_UNIFORM(out_k);
+            PM_UNIFORM(out_a);
             c.allocated += (long long)(out_k & kSizeMask);
             c.peak_reserved = max(c.peak_reserved, c.reserved);
             c.peak_allocated = max(c.peak_allocated, c.allocated);
-            c.maxF = max(c.maxF, c.F);
             st.a[j] = out_a;  // uniform stores
             st.k[j] = out_k;
             st.L[j] = out_L;
@@ -902,91 +976,7 @@ __device__ __forceinline__ void replay_trace(
               rp[2] = (u64)out_L;
               rp[3] = (u64)out_R;
             }
-          }
-        }
-      } else {
-        // free (allocator.py:294-320): double free before unknown handle
-        const u64 rkj = st.k[src];
-        PM_UNIFORM(rkj);
-        PM_UNIFORM(st.a[src]);
-        PM_UNIFORM(st.L[src]);
-        PM_UNIFORM(st.R[src]);
-        if (rkj == kFreed) {
-          sts = PM_DOUBLE_FREE;
-        } else if (rkj == 0) {
-          sts = PM_UNKNOWN_HANDLE;
-        } else {
-          const u64 A = st.a[src];
-          const u32 L = st.L[src], R = st.R[src];
-          const u64 S = rkj & kSizeMask;
-          c.allocated -= (long long)S;
-          const bool lf = is_free_ref(L), rf = is_free_ref(R);
-          if (!lf && !rf) {
-            const int id = pool_insert(P, dir, c, rkj, A, mk_links(L, R), rec,
-                                       st, hcmp, lane);
-            if (id < 0) {
-              sts = PM_POOL_OVERFLOW;
-            } else {
-              if (L != kNone)
-                set_link(rec, st, hcmp, lane, L, 1, kFreeTag | (u32)id);
-              if (R != kNone)
-                set_link(rec, st, hcmp, lane, R, 0, kFreeTag | (u32)id);
-            }
-          } else if (lf && !rf) {
-            // the free block on the left absorbs this one
-            const int pid = (int)(L & ~kFreeTag);
-            const u64 pk = P.key[pid];
-            const u64 pa = P.addr[pid];
-            const u32 pL = lo32(P.links[pid]);
-            __syncwarp();
-            P.links[pid] = mk_links(pL, R);
-            const int nid =
-                pool_rekey(P, dir, c, pid, pk + S, pa, rec, st, hcmp, lane);
-            if (nid < 0) {
-              sts = PM_POOL_OVERFLOW;
-            } else if (nid == pid && R != kNone) {
-              set_link(rec, st, hcmp, lane, R, 0, kFreeTag | (u32)nid);
-            }
-          } else if (!lf && rf) {
-            // the free block on the right absorbs this one
-            const int rid = (int)(R & ~kFreeTag);
-            const u64 rk2 = P.key[rid];
-            const u32 rR = hi32(P.links[rid]);
-            __syncwarp();
-            P.links[rid] = mk_links(L, rR);
-            const int nid =
-                pool_rekey(P, dir, c, rid, rk2 + S, A, rec, st, hcmp, lane);
-            if (nid < 0) {
-              sts = PM_POOL_OVERFLOW;
-            } else if (nid == rid && L != kNone) {
-              set_link(rec, st, hcmp, lane, L, 1, kFreeTag | (u32)nid);
-            }
           } else {
-            // left absorbs this block and the right free block
-            int pid = (int)(L & ~kFreeTag);
-            const int rid = (int)(R & ~kFreeTag);
-            const u64 rk2 = P.key[rid];
-            const u32 rR = hi32(P.links[rid]);
-            const int moved =
-                pool_remove(P, dir, c, rid, rec, st, hcmp, lane);
-            if (moved == pid) pid = rid;
-            const u64 pk = P.key[pid];
-            const u64 pa = P.addr[pid];
-            const u32 pL = lo32(P.links[pid]);
-            __syncwarp();
-            P.links[pid] = mk_links(pL, rR);
-            const int nid = pool_rekey(P, dir, c, pid,
-                                       pk + S + (rk2 & kSizeMask), pa, rec,
-                                       st, hcmp, lane);
-            if (nid < 0) {
-              sts = PM_POOL_OVERFLOW;
-            } else if (nid == pid && rR != kNone) {
-              set_link(rec, st, hcmp, lane, rR, 0, kFreeTag | (u32)nid);
-            }
-          }
-          if (sts == PM_OK) {
-            c.maxF = max(c.maxF, c.F);
-            __syncwarp();
             st.k[j] = kFreed;  // uniform store
             if (lane == j) *rec.word((u32)hj, 1) = kFreed;
           }
@@ -1034,8 +1024,7 @@ __device__ __forceinline__ void replay_trace(
 
 struct Ctl {
   unsigned work[4];   // work counters: main pass, tiers 1, 2 and 3
-  unsigned n_list[4]; // [1]: in-warp HBM re-runs (count); [2], [3]: traces
-                      // queued for the tier-2 / tier-3 kernels
+  unsigned n_list[4]; // traces queued for tier 1 / 2 / 3 (index 1..3)
   unsigned pad[56];
 };
 
@@ -1052,10 +1041,6 @@ __host__ __device__ __forceinline__ size_t gmem_warp_bytes(int nbmax) {
   return ((size_t)nbmax * kBucket * 24 + 32 * 24 + (size_t)nbmax * 32 + 255) /
          256 * 256;
 }
-
-// Per-warp private overflow pool of the main kernel (HBM, L2-resident):
-// 32 buckets of entries plus the in-use word its DirReg allocates from.
-constexpr size_t kHpoolWarpBytes = (size_t)kBucket * kBucket * 24 + 256;
 
 __device__ __forceinline__ void carve_pool(char* base, int nbuckets, Pool& P) {
   const size_t E = (size_t)nbuckets * kBucket;
@@ -1088,8 +1073,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
                        int pass, const int32_t* __restrict__ list, int n_host,
                        int32_t* __restrict__ overflow_list, int buckets,
                        const unsigned* __restrict__ group_end, int n_groups,
-                       const volatile unsigned* ready,
-                       char* __restrict__ hpool) {
+                       const volatile unsigned* ready) {
   extern __shared__ __align__(16) char smem[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
@@ -1127,27 +1111,8 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
     replay_trace(tr, reqs, offs, cfgs, cfg_of, results, timeline, recs, P,
                  dir, kBucket, st, lane);
     __syncwarp();
-    int sts = __shfl_sync(kFull, lane == 0 ? results[tr].status : 0, 0);
-    if (sts == PM_POOL_OVERFLOW && hpool != nullptr) {
-      // the CTA's shared pool ran dry (or the trace needs > 32 buckets):
-      // re-run at once in this warp over its private 32-bucket HBM pool
-      if (lane == 0) atomicAdd(&ctl->n_list[1], 1u);  // diagnostic count
-      char* hb = hpool + ((size_t)blockIdx.x * WARPS + wib) * kHpoolWarpBytes;
-      Pool HP;
-      carve_pool(hb, kBucket, HP);
-      DirReg hdir;
-      hdir.cta_used = reinterpret_cast<unsigned*>(hb + (size_t)kBucket * kBucket * 24);
-      hdir.cta_words = 1;
-      hdir.cta_buckets = kBucket;
-      if (lane == 0) *hdir.cta_used = 0u;
-      __syncwarp();
-      replay_trace(tr, reqs, offs, cfgs, cfg_of, results, timeline, recs, HP,
-                   hdir, kBucket, st, lane);
-      __syncwarp();
-      sts = __shfl_sync(kFull, lane == 0 ? results[tr].status : 0, 0);
-    }
-    if (lane == 0 && sts == PM_POOL_OVERFLOW) {
-      const unsigned k = atomicAdd(&ctl->n_list[2], 1u);  // tier-2 queue
+    if (lane == 0 && results[tr].status == PM_POOL_OVERFLOW) {
+      const unsigned k = atomicAdd(&ctl->n_list[pass + 1], 1u);
       overflow_list[k] = tr;
     }
   }

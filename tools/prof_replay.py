@@ -37,7 +37,7 @@ def main():
         res = batch.results()
         ev = int(res["n_events_replayed"].sum())
         ctl = batch.d_ws[:32].cpu().numpy().view(np.uint32)
-        print(f"in-warp HBM re-runs {ctl[5]}, tier-2 {ctl[6]}, tier-3 {ctl[7]} traces")
+        print(f"tier-1 {ctl[5]}, tier-2 {ctl[6]}, tier-3 {ctl[7]} retries")
         print(f"{args.traces} traces {ev} events {dt*1e3:.1f} ms "
               f"{ev/dt/1e9:.3f} Gev/s maxF {res['max_free_blocks'].max()} "
               f"status {set(res['status'].tolist())}")
