@@ -135,10 +135,20 @@ def cpu_baseline(reqs, offsets, cfg, stride: int, gpu_results=None):
     res, _ = oracle.replay_batch(sub, sub_offs, cfg, n_threads=threads)
     dt = time.perf_counter() - t0
     events = int(res["n_events_replayed"].sum())
+    # SURVEY §8d also asks for a 1-core figure: every 10th trace of the sample
+    k1 = max(1, len(idx) // 10)
+    t1 = time.perf_counter()
+    r1, _ = oracle.replay_batch(sub[:sub_offs[k1]], sub_offs[:k1 + 1], cfg,
+                                n_threads=1)
+    dt1 = time.perf_counter() - t1
+    ev1 = int(r1["n_events_replayed"].sum())
     out = {"value": events / dt, "unit": "events/s", "cores": threads,
            "kind": "port",
            "sample": f"every {stride}th trace of the rank-0 shard: "
-                     f"{len(idx)} traces, {events} requests, {dt:.2f} s wall"}
+                     f"{len(idx)} traces, {events} requests, {dt:.2f} s wall",
+           "value_1core": ev1 / dt1,
+           "sample_1core": f"first {k1} traces of that sample, {ev1} requests, "
+                           f"{dt1:.2f} s on 1 thread"}
     parity = None
     if gpu_results is not None:
         mism = int((gpu_results[idx] != res).sum())
@@ -263,14 +273,17 @@ def main():
     achieved = events_per_step * BYTES_PER_EVENT / mean_launch_s / 1e9
     peak, peak_kind = read_peak()
     traffic = None
+    issue = None
     prof = REPO / "profiles" / "replay_ncu_summary.json"
     if prof.exists():
-        try:
-            traffic = json.loads(prof.read_text()).get("dram_bytes_per_event")
-            if traffic is not None:
-                traffic = traffic * events_per_step
-        except Exception:
-            traffic = None
+        summ = json.loads(prof.read_text())
+        # same unit as `achieved`: DRAM bytes per launch / launch time
+        traffic = summ["dram_bytes_per_event"] * events_per_step / mean_launch_s / 1e9
+        # the real bound is issue -- SMs x 4 schedulers x clock /
+        # warp-instructions per event (ncu-measured, profiles/)
+        sms = torch.cuda.get_device_properties(dev).multi_processor_count
+        issue = {"warp_instructions_per_event": summ["warp_instructions_per_event"],
+                 "sms": sms, "schedulers_per_sm": 4}
 
     if rank != 0:
         if dist:
@@ -316,13 +329,24 @@ def main():
                      "unit": "GB/s", "frac": achieved / peak,
                      "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
                      "traffic": traffic,
-                     "kernel": "replay_smem_kernel (main pass; tier-1 / tier-2 retry kernels ride in the same timed launch)",
+                     "traffic_note": "GB/s: DRAM read+write bytes per event from the ncu "
+                                     "--set full capture (profiles/replay_ncu_summary.json) "
+                                     "x events per launch / launch time",
+                     "kernel": "replay_smem_kernel (main pass; the tier-1/2/3 retry kernels ride in the same timed launch)",
                      "algorithmic_bytes_per_event": BYTES_PER_EVENT},
         "cpu_baseline": cpu,
         "parity": parity,
         "clocks": clocks.summary(),
+        "issue_bound": issue,
         "gpu_launches": 3 * args.steps,
     }
+    if issue is not None:
+        mhz = line["clocks"]["sm_mhz"] or 1965.0
+        ceiling = issue["sms"] * 4 * mhz * 1e6 / issue["warp_instructions_per_event"]
+        issue.update({"clock_mhz": mhz, "ceiling_events_per_s": ceiling,
+                      "frac": value / (ceiling * world),
+                      "source": "profiles/replay_ncu_summary.json (ncu --set full "
+                                "of the replay kernel: instructions, DRAM bytes)"})
     print(json.dumps(line))
     if dist:
         dist.destroy_process_group()

@@ -98,7 +98,8 @@ typedef enum {
   PM_ERR_INVALID_ARGUMENT = 1,
   PM_ERR_CUDA = 2,
   PM_ERR_WORKSPACE_TOO_SMALL = 3,
-  PM_ERR_NO_DEVICE = 4
+  PM_ERR_NO_DEVICE = 4,
+  PM_ERR_CYCLIC_PARENT = 5   /* pm_layer_tree: -> CyclicParentLink */
 } pm_err_t;
 
 const char* pm_last_error(void);

@@ -19,6 +19,8 @@
  *   pm_link_roots  -> linking.link on caller-given roots and blocks
  *   pm_orchestrate -> orchestration.build_sequence's per-block rewrites,
  *                     emission and total order (orchestration.py:270-387)
+ *   pm_layer_tree  -> analysis.build_layer_tree's ancestor walk, child
+ *                     order and walk order (analysis.py:113-182)
  */
 #ifndef PEAKMEM_PIPELINE_H
 #define PEAKMEM_PIPELINE_H
@@ -75,6 +77,27 @@ int pm_orchestrate(int64_t nb, const int64_t* b_alloc, const int64_t* b_size,
                    int64_t* o_vts, int32_t* o_tag, int64_t* o_a, int64_t* o_b,
                    int32_t* o_role, pm_req_t* o_packed, int32_t* fb_role,
                    int64_t* fb_free, int32_t* fb_flags, void* stream);
+
+/* pm_layer_tree -> analysis.build_layer_tree (analysis.py:113-182), the
+ * structural part: n python_function frames in event order (python id /
+ * parent id, INT64_MIN = None; is_layer = the name matches a layer prefix;
+ * start).  Duplicate ids keep the first frame; each layer frame's nearest
+ * layer ancestor follows the reference's parent walk (a chain that revisits
+ * the walker's own id, or does not terminate, returns
+ * PM_ERR_CYCLIC_PARENT).  event_id (nullable) breaks start ties; NULL =
+ * input order.  Outputs over the n_layers layer frames (their
+ * order = event order): node_parent (index or -1 = the synthetic root),
+ * child_order + child_off (n_layers+2; slot 0 = root, slot v+1 = node v):
+ * children sorted by (start, event id), and walk[0..*n_walk): the pre-order
+ * walk from the root (LayerNode.walk without the root).  Layer frames that
+ * are each other's nearest layer ancestors (a cycle the reference's walk
+ * does not flag) are reachable from no root path and not in the walk. */
+int pm_layer_tree(int64_t n, const int64_t* pid, const int64_t* par,
+                  const uint8_t* is_layer, const int64_t* start,
+                  const int64_t* event_id, int64_t n_layers,
+                  int64_t* node_parent,
+                  int64_t* child_order, int64_t* child_off, int64_t* walk,
+                  int64_t* n_walk, void* stream);
 
 #ifdef __cplusplus
 }

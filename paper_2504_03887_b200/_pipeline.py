@@ -14,7 +14,8 @@ from .errors import EngineUnavailable
 
 LIB_PATH = LIB_DIR / "libpeakmem_pipeline.so"
 EXPORTED_SYMBOLS = ("pm_pipeline_last_error", "pm_sort_events", "pm_link",
-                    "pm_link_roots", "pm_orchestrate")
+                    "pm_link_roots", "pm_orchestrate", "pm_layer_tree")
+PM_ERR_CYCLIC_PARENT = 5
 NONE = np.iinfo(np.int64).min
 
 _lib = None
@@ -72,6 +73,34 @@ def sort_events(ts: np.ndarray, dur: np.ndarray):
                               _p(start), _p(duration),
                               ctypes.c_void_p(_stream())), lib)
     return perm, start, duration
+
+
+def layer_tree(pid, par, is_layer, start, event_id=None):
+    """Device layer tree over python_function frames in event order
+    (pm_layer_tree; analysis.py:113-182).  Returns (node_parent,
+    child_order, child_off, walk) over the layer frames; raises
+    CyclicParentLink like the reference's walk."""
+    from .errors import CyclicParentLink
+    lib = load()
+    _native.require_device()
+    pid, par, start = _i64(pid), _i64(par), _i64(start)
+    eid = None if event_id is None else _i64(event_id)
+    flag = np.ascontiguousarray(is_layer, dtype=np.uint8)
+    n = len(pid)
+    nl = int(flag.sum())
+    node_parent = np.empty(max(nl, 1), np.int64)
+    child_order = np.empty(max(nl, 1), np.int64)
+    child_off = np.zeros(nl + 2, np.int64)
+    walk = np.empty(max(nl, 1), np.int64)
+    n_walk = ctypes.c_int64(0)
+    rc = lib.pm_layer_tree(ctypes.c_int64(n), _p(pid), _p(par), _p(flag),
+                           _p(start), _p(eid), ctypes.c_int64(nl), _p(node_parent),
+                           _p(child_order), _p(child_off), _p(walk),
+                           ctypes.byref(n_walk), ctypes.c_void_p(_stream()))
+    if rc == PM_ERR_CYCLIC_PARENT:
+        raise CyclicParentLink(lib.pm_pipeline_last_error().decode(errors="replace"))
+    _check(rc, lib)
+    return node_parent[:nl], child_order[:nl], child_off, walk[:n_walk.value]
 
 
 class LinkResult:

@@ -115,56 +115,43 @@ def build_layer_tree(functions: list[TraceEvent],
                      ) -> LayerNode:
     """Module-call frames as a tree (analysis.py:115-182): non-layer frames
     collapse, each layer hangs under its nearest layer ancestor through the
-    python parent chain (first python id wins, cycles raise)."""
+    python parent chain (first python id wins, cycles raise) -- the walk,
+    child order and pre-order on the device (pm_layer_tree)."""
     for e in functions:
         if e.category is not EventCategory.PYTHON_FUNCTION:
             raise ValueError(f"not a python_function event: {e.name!r}")
-    first: dict[int, TraceEvent] = {}
+    seen: set[int] = set()
     for e in functions:
-        if e.python_id is None:
-            continue
-        if e.python_id in first:
-            logger.warning("duplicate python id %s (%r); keeping the first",
-                           e.python_id, e.name)
-            continue
-        first[e.python_id] = e
-
-    def nearest_layer(e: TraceEvent) -> TraceEvent | None:
-        visited = set() if e.python_id is None else {e.python_id}
-        node = e
-        while node.parent_id is not None:
-            up = first.get(node.parent_id)
-            if up is None:
-                return None
-            if up.python_id in visited:
-                raise CyclicParentLink(
-                    f"parent chain of {e.name!r} revisits id {up.python_id}")
-            visited.add(up.python_id)
-            if _is_layer(up.name, layer_prefixes):
-                return up
-            node = up
-        return None
-
-    root = LayerNode(name="<root>", start_ts=0, end_ts=0, is_wrapper=True)
-    layers = [e for e in functions if _is_layer(e.name, layer_prefixes)]
-    nodes: dict[int, LayerNode] = {}
+        if e.python_id is not None:
+            if e.python_id in seen:
+                logger.warning("duplicate python id %s (%r); keeping the first",
+                               e.python_id, e.name)
+            seen.add(e.python_id)
+    none = _pipeline.NONE
+    is_layer = np.array([_is_layer(e.name, layer_prefixes) for e in functions],
+                        bool)
+    node_parent, order, off, _walk = _pipeline.layer_tree(
+        [none if e.python_id is None else e.python_id for e in functions],
+        [none if e.parent_id is None else e.parent_id for e in functions],
+        is_layer, [e.start_ts for e in functions],
+        [e.event_id for e in functions])
+    layers = [e for e, f in zip(functions, is_layer.tolist()) if f]
+    nodes = []
     for e in layers:
         shown = e.name
         for prefix in layer_prefixes:
             if shown.startswith(prefix):
                 shown = shown[len(prefix):]
                 break
-        nodes[e.event_id] = LayerNode(name=shown, start_ts=e.start_ts,
-                                      end_ts=e.end_ts, event_id=e.event_id)
-    for e in layers:
-        anc = nearest_layer(e)
-        (nodes[anc.event_id] if anc is not None else root).children.append(
-            nodes[e.event_id])
-    order = lambda n: (n.start_ts, n.event_id)  # noqa: E731
-    for node in nodes.values():
-        node.children.sort(key=order)
+        nodes.append(LayerNode(name=shown, start_ts=e.start_ts, end_ts=e.end_ts,
+                               event_id=e.event_id))
+    root = LayerNode(name="<root>", start_ts=0, end_ts=0, is_wrapper=True)
+    o = order.tolist()
+    off = off.tolist()
+    root.children = [nodes[v] for v in o[off[0]:off[1]]]
+    for k, node in enumerate(nodes):
+        node.children = [nodes[v] for v in o[off[k + 1]:off[k + 2]]]
         node.is_wrapper = bool(node.children)
-    root.children.sort(key=order)
     if root.children:
         root.start_ts = min(c.start_ts for c in root.children)
         root.end_ts = max(c.end_ts for c in root.children)
@@ -266,12 +253,12 @@ def group_memory_events(instants: list[TraceEvent]) -> list[MemoryBlock]:
 class LayerTreeColumns:
     """The layer tree of analysis.py:115-182 computed from bundle columns.
 
-    Nearest-layer ancestors come from a vectorised parent-pointer walk
-    (first python id wins; a chain that returns to its own layer or never
-    terminates raises CyclicParentLink, as the reference's seen-set does);
-    children are ordered by (start, event_id); the pre-order walk gives the
-    non-wrapper layers (leaves) the link kernels consume.  LayerNode
-    objects are built only on demand (`tree()`).
+    Nearest-layer ancestors, the (start, event_id) child order and the
+    pre-order walk come from `pm_layer_tree` on the device (first python id
+    wins; a chain that returns to its own id or never terminates raises
+    CyclicParentLink, as the reference's seen-set does); the walk gives the
+    non-wrapper layers (leaves) the link kernels consume.  LayerNode objects
+    are built only on demand (`tree()`).
     """
 
     def __init__(self, bundle):
@@ -288,75 +275,20 @@ class LayerTreeColumns:
         else:
             is_layer = np.fromiter((_is_layer(names[i], LAYER_NAME_PREFIXES)
                                     for i in idx.tolist()), bool, len(idx))
-        n = len(idx)
-        from .trace import NONE as NO
-        # first occurrence of every python id
-        valid = pid != NO
-        order = np.argsort(pid, kind="stable")
-        spid = pid[order]
-        first = np.ones(n, bool)
-        first[1:] = spid[1:] != spid[:-1]
-        u_pid = spid[first & (spid != NO)]
-        u_pos = order[first & (spid != NO)]
-        pos = np.searchsorted(u_pid, par)
-        pos = np.clip(pos, 0, max(len(u_pid) - 1, 0))
-        has = (par != NO) & (len(u_pid) > 0)
-        if len(u_pid):
-            has &= u_pid[pos] == par
-        parent_pos = np.where(has, u_pos[pos] if len(u_pid) else -1, -1)
-        del valid
         lay = np.nonzero(is_layer)[0]
-        anc = np.full(len(lay), -2, np.int64)  # -2 unresolved, -1 root
-        cur = parent_pos[lay]
-        active = np.ones(len(lay), bool)
-        for _ in range(n + 2):
-            if not active.any():
-                break
-            a = np.nonzero(active)[0]
-            c = cur[a]
-            root = c < 0
-            anc[a[root]] = -1
-            active[a[root]] = False
-            a, c = a[~root], c[~root]
-            own = pid[lay[a]]
-            selfhit = (c == lay[a]) | ((own != NO) & (pid[c] == own))
-            if selfhit.any():
-                raise CyclicParentLink("parent chain revisits its own layer")
-            hit = is_layer[c]
-            anc[a[hit]] = c[hit]
-            active[a[hit]] = False
-            cur[a[~hit]] = parent_pos[c[~hit]]
-        else:
-            raise CyclicParentLink("parent chain does not terminate")
-        if active.any():
-            raise CyclicParentLink("parent chain does not terminate")
-        # nodes: the layer events (positions within idx)
+        # ancestor walk, child order and pre-order walk on the device
+        # (pm_layer_tree); the layer-name test above stays on the host
+        (self.node_parent, o, self.child_off,
+         self.walk) = _pipeline.layer_tree(pid, par, is_layer,
+                                           bundle.start[idx])
         self.node_event = idx[lay]
         self.node_start = bundle.start[self.node_event]
         self.node_end = bundle.end[self.node_event]
-        self.node_name = [names[i] for i in self.node_event.tolist()]
-        lay_index = np.full(n, -1, np.int64)
-        lay_index[lay] = np.arange(len(lay))
-        self.node_parent = np.where(anc >= 0, lay_index[np.maximum(anc, 0)], -1)
-        # children ordered by (start, event_id): sort by (parent, start, id)
-        o = np.lexsort((self.node_event, self.node_start, self.node_parent))
+        self.node_name = names.take(self.node_event) if hasattr(names, "take") \
+            else [names[i] for i in self.node_event.tolist()]
         self.child_order = o
-        par_sorted = self.node_parent[o]
-        nn = len(lay)
-        counts = np.bincount(par_sorted + 1, minlength=nn + 1)
-        self.child_off = np.zeros(nn + 2, np.int64)
-        np.cumsum(counts, out=self.child_off[1:])
-        self.is_wrapper = counts[1:] > 0
-        # pre-order walk from the synthetic root (parent -1 -> slot 0)
-        walk = []
-        stack = list(reversed(o[self.child_off[0]:self.child_off[1]].tolist()))
-        off = self.child_off
-        while stack:
-            v = stack.pop()
-            walk.append(v)
-            stack.extend(reversed(o[off[v + 1]:off[v + 2]].tolist()))
-        self.walk = np.array(walk, np.int64)
-        leaves = self.walk[~self.is_wrapper[self.walk]] if len(walk) else self.walk
+        self.is_wrapper = np.diff(self.child_off)[1:] > 0
+        leaves = self.walk[~self.is_wrapper[self.walk]] if len(lay) else self.walk
         self.leaves = leaves
         self.leaf_start = self.node_start[leaves]
         self.leaf_end = self.node_end[leaves]

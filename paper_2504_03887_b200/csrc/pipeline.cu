@@ -24,6 +24,7 @@
 #include <stdint.h>
 
 #include <cub/cub.cuh>
+#include <algorithm>
 #include <string>
 #include <vector>
 
@@ -157,6 +158,178 @@ __global__ void k_seq_keys(const long long* op_root, const long long* seq,
   const long long s = seq[i];
   valid[i] = s >= 0 ? 1 : 0;
   keys[i] = ((u64)op_root[i] << 32) | (u64)(s & 0xffffffffll);
+}
+
+// ---- a4: layer tree (analysis.py:113-182) --------------------------------------
+
+// first occurrence of every python id: keys sorted stably by id, the first
+// of each run kept (analysis.py:126-134: duplicates keep the first)
+__global__ void k_pid_keys(const long long* pid, long long n, u64* keys,
+                           long long* idx) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  keys[i] = (u64)pid[i] ^ 0x8000000000000000ull;  // order-preserving bias
+  idx[i] = i;
+}
+
+__global__ void k_pid_first(const u64* skeys, long long n, int* first) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const bool none = skeys[i] == 0ull;  // INT64_MIN (None) biased to 0
+  first[i] = !none && (i == 0 || skeys[i] != skeys[i - 1]) ? 1 : 0;
+}
+
+__global__ void k_pid_parent(const long long* par, long long n,
+                             const u64* ukeys, const long long* upos,
+                             long long nu, long long* parent_pos) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const long long p = par[i];
+  long long r = -1;
+  if (p != kNoneTs && nu > 0) {
+    const u64 k = (u64)p ^ 0x8000000000000000ull;
+    const long long j = lower_bound_ll(ukeys, nu, k);
+    if (j < nu && ukeys[j] == k) r = upos[j];
+  }
+  parent_pos[i] = r;
+}
+
+// nearest layer ancestor of every layer frame: the reference's walk
+// (analysis.py:136-151) one parent at a time -- a chain that reaches a
+// frame with the walker's own python id (its own frame included) or runs
+// longer than n steps revisits an id: CyclicParentLink (flagged).
+__global__ void k_layer_anc(const long long* lay, long long nl,
+                            const long long* pid, const long long* parent_pos,
+                            const unsigned char* is_layer,
+                            const long long* lay_index, long long n,
+                            long long* node_parent, int* cyclic) {
+  long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (v >= nl) return;
+  const long long e = lay[v];
+  const long long own = pid[e];
+  long long c = parent_pos[e];
+  long long steps = 0;
+  long long anc = -1;
+  while (c >= 0) {
+    if (c == e || (own != kNoneTs && pid[c] == own) || ++steps > n) {
+      atomicExch(cyclic, 1);
+      anc = -1;
+      break;
+    }
+    if (is_layer[c]) {
+      anc = lay_index[c];
+      break;
+    }
+    c = parent_pos[c];
+  }
+  node_parent[v] = anc;
+}
+
+// CSR offsets of children per parent slot (slot 0 = the synthetic root):
+// off[p] = first index in the (parent, start, event)-sorted order
+__global__ void k_child_off(const unsigned* sorted_parent_key, long long nl,
+                            long long* off) {
+  long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (k > nl + 1) return;
+  off[k] = lower_bound_ll(sorted_parent_key, nl, (unsigned)k);
+}
+
+// level offsets of depth-sorted nodes: lvl[d] = first node of depth >= d
+__global__ void k_level_off(const int* sorted_depth, long long nl, int maxd,
+                            long long* lvl) {
+  int d = blockIdx.x * blockDim.x + threadIdx.x;
+  if (d > maxd + 1) return;
+  lvl[d] = lower_bound_ll(sorted_depth, nl, d);
+}
+
+// depth by pointer jumping (list ranking over parent links)
+__global__ void k_depth_init(const long long* node_parent, long long nl,
+                             long long* jump, int* depth) {
+  long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (v >= nl) return;
+  jump[v] = node_parent[v];
+  depth[v] = node_parent[v] >= 0 ? 1 : 0;
+}
+
+__global__ void k_depth_step(const long long* jump_in, const int* depth_in,
+                             long long nl, long long* jump_out, int* depth_out) {
+  long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (v >= nl) return;
+  const long long j = jump_in[v];
+  if (j >= 0) {
+    depth_out[v] = depth_in[v] + depth_in[j];
+    jump_out[v] = jump_in[j];
+  } else {
+    depth_out[v] = depth_in[v];
+    jump_out[v] = -1;
+  }
+}
+
+// a chain that never reached the root runs into a cycle of layer frames
+// (each the other's nearest layer ancestor -- not an error for the
+// reference): such nodes hang off no root path and are left out of the walk
+__global__ void k_depth_final(const long long* jump, long long nl, int* depth) {
+  long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (v < nl && jump[v] != -1) depth[v] = -1;
+}
+
+// subtree sizes, one depth level at a time from the deepest
+__global__ void k_subtree_level(const long long* lvl_nodes, long long m,
+                                const long long* child_order,
+                                const long long* off, long long* size) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  const long long v = lvl_nodes[i];
+  long long s = 1;
+  for (long long k = off[v + 1]; k < off[v + 2]; ++k) s += size[child_order[k]];
+  size[v] = s;
+}
+
+// pre-order positions, one level at a time from the top: children of v
+// take consecutive ranges after pre[v] in (start, event) order
+__global__ void k_preorder_level(const long long* lvl_nodes, long long m,
+                                 const long long* child_order,
+                                 const long long* off, const long long* size,
+                                 long long* pre) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  const long long v = lvl_nodes[i];  // -1: the synthetic root
+  long long next = v >= 0 ? pre[v] + 1 : 0;
+  for (long long k = off[v + 1]; k < off[v + 2]; ++k) {
+    const long long c = child_order[k];
+    pre[c] = next;
+    next += size[c];
+  }
+}
+
+__global__ void k_scatter_walk(const long long* nodes, long long m,
+                               const long long* pre, long long* walk) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i < m) walk[pre[nodes[i]]] = nodes[i];
+}
+
+__global__ void k_u8_to_int(const unsigned char* f, long long n, int* out) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i < n) out[i] = f[i] ? 1 : 0;
+}
+
+__global__ void k_scatter_flagged(const int* flag, const long long* pos,
+                                  long long n, long long* out) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i < n && flag[i]) out[pos[i]] = i;
+}
+
+__global__ void k_gather_parent_key(const long long* node_parent,
+                                    const long long* ord, long long nl,
+                                    unsigned* keys) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i < nl) keys[i] = (unsigned)(node_parent[ord[i]] + 1);
+}
+
+__global__ void k_gather_u64_idx(const u64* src, const long long* idx,
+                                 long long n, u64 bias, u64* out) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i < n) out[i] = src[idx[i]] + bias;
 }
 
 // ---- a7: grouping -------------------------------------------------------------
@@ -1440,6 +1613,181 @@ int pm_orchestrate(int64_t nb, const int64_t* b_alloc, const int64_t* b_size,
   }
   *n_req_out = n_raw;
   return PM_SUCCESS;
+}
+
+// ---- a4 / f4: the layer tree on the device ----------------------------------
+
+int pm_layer_tree(int64_t n, const int64_t* pid, const int64_t* par,
+                  const uint8_t* is_layer, const int64_t* start,
+                  const int64_t* event_id, int64_t n_layers,
+                  int64_t* node_parent,
+                  int64_t* child_order, int64_t* child_off, int64_t* walk,
+                  int64_t* n_walk, void* stream_) {
+  if (n < 0 || n_layers < 0 || n_layers > n ||
+      (n > 0 && (!pid || !par || !is_layer || !start)) ||
+      (n_layers > 0 && (!node_parent || !child_order || !child_off || !walk)))
+    return perr(PM_ERR_INVALID_ARGUMENT, "pm_layer_tree: bad arguments");
+  if (child_off) {
+    child_off[0] = 0;
+    if (n_layers == 0) child_off[1] = 0;
+  }
+  if (n_walk) *n_walk = 0;
+  if (n_layers == 0) return PM_SUCCESS;
+  cudaStream_t s = (cudaStream_t)stream_;
+  const long long nl = n_layers;
+  Arena A(s);
+  const long long* d_pid = (const long long*)A.upload(pid, n);
+  const long long* d_par = (const long long*)A.upload(par, n);
+  const unsigned char* d_isl = A.upload(is_layer, n);
+  const long long* d_start = (const long long*)A.upload(start, n);
+  // python id -> first frame
+  u64* keys = A.alloc<u64>(n);
+  u64* skeys = A.alloc<u64>(n);
+  long long* idx = A.alloc<long long>(n);
+  long long* sidx = A.alloc<long long>(n);
+  int* first = A.alloc<int>(n);
+  u64* ukeys = A.alloc<u64>(n);
+  long long* upos = A.alloc<long long>(n);
+  long long* nsel = A.alloc<long long>(1);
+  long long* parent_pos = A.alloc<long long>(n);
+  // layer frames
+  int* lflag = A.alloc<int>(n);
+  long long* lay_index = A.alloc<long long>(n);
+  long long* lay = A.alloc<long long>(nl);
+  long long* d_np = A.alloc<long long>(nl);
+  int* cyclic = A.alloc<int>(1);
+  unsigned* pkey = A.alloc<unsigned>(nl);
+  unsigned* pkey2 = A.alloc<unsigned>(nl);
+  u64* skey = A.alloc<u64>(nl);
+  u64* skey2 = A.alloc<u64>(nl);
+  long long* ord = A.alloc<long long>(nl);
+  long long* ord2 = A.alloc<long long>(nl);
+  long long* off = A.alloc<long long>(nl + 2);
+  long long* jump[2] = {A.alloc<long long>(nl), A.alloc<long long>(nl)};
+  int* depth[2] = {A.alloc<int>(nl), A.alloc<int>(nl)};
+  int* sdepth = A.alloc<int>(nl);
+  long long* by_depth = A.alloc<long long>(nl);
+  long long* nodes = A.alloc<long long>(nl);
+  int* dmax = A.alloc<int>(1);
+  long long* size = A.alloc<long long>(nl);
+  long long* pre = A.alloc<long long>(nl);
+  long long* d_walk = A.alloc<long long>(nl);
+  long long* minus1 = A.alloc<long long>(1);
+  if (A.err != cudaSuccess) return perr(PM_ERR_CUDA, "pm_layer_tree: alloc");
+  size_t tmp = 0, t2 = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, tmp, keys, skeys, idx, sidx, (int64_t)n, 0, 64, s);
+  cub::DeviceSelect::Flagged(nullptr, t2, skeys, first, ukeys, nsel, (int64_t)n, s);
+  tmp = std::max(tmp, t2);
+  cub::DeviceScan::ExclusiveSum(nullptr, t2, lflag, lay_index, (int64_t)n, s);
+  tmp = std::max(tmp, t2);
+  cub::DeviceRadixSort::SortPairs(nullptr, t2, skey, skey2, ord, ord2, (int64_t)nl, 0, 64, s);
+  tmp = std::max(tmp, t2);
+  cub::DeviceRadixSort::SortPairs(nullptr, t2, depth[0], sdepth, ord, by_depth, (int64_t)nl, 0, 32, s);
+  tmp = std::max(tmp, t2);
+  cub::DeviceReduce::Max(nullptr, t2, depth[0], dmax, (int64_t)nl, s);
+  tmp = std::max(tmp, t2);
+  void* t = A.alloc<char>(tmp);
+  if (A.err != cudaSuccess) return perr(PM_ERR_CUDA, "pm_layer_tree: alloc");
+
+  pmp::k_pid_keys<<<blocks_for(n), 256, 0, s>>>(d_pid, n, keys, idx);
+  cub::DeviceRadixSort::SortPairs(t, tmp, keys, skeys, idx, sidx, (int64_t)n, 0, 64, s);
+  pmp::k_pid_first<<<blocks_for(n), 256, 0, s>>>(skeys, n, first);
+  cub::DeviceSelect::Flagged(t, tmp, skeys, first, ukeys, nsel, (int64_t)n, s);
+  cub::DeviceSelect::Flagged(t, tmp, sidx, first, upos, nsel, (int64_t)n, s);
+  long long nu = 0;
+  int rc = download(&nu, nsel, 1, s);
+  if (rc == PM_SUCCESS) rc = sync_check(s, "pm_layer_tree: ids");
+  if (rc != PM_SUCCESS) return rc;
+  pmp::k_pid_parent<<<blocks_for(n), 256, 0, s>>>(d_par, n, ukeys, upos, nu,
+                                                   parent_pos);
+  // layer positions and their index among layers (input is in event order)
+  pmp::k_u8_to_int<<<blocks_for(n), 256, 0, s>>>(d_isl, n, lflag);
+  cub::DeviceScan::ExclusiveSum(t, tmp, lflag, lay_index, (int64_t)n, s);
+  pmp::k_scatter_flagged<<<blocks_for(n), 256, 0, s>>>(lflag, lay_index, n, lay);
+  cudaMemsetAsync(cyclic, 0, sizeof(int), s);
+  pmp::k_layer_anc<<<blocks_for(nl), 256, 0, s>>>(lay, nl, d_pid, parent_pos,
+                                                   d_isl, lay_index, n, d_np,
+                                                   cyclic);
+  int h_cyc = 0;
+  rc = download(&h_cyc, cyclic, 1, s);
+  if (rc == PM_SUCCESS) rc = sync_check(s, "pm_layer_tree: ancestors");
+  if (rc != PM_SUCCESS) return rc;
+  if (h_cyc) return perr(PM_ERR_CYCLIC_PARENT, "parent chain revisits a python id");
+  // children in (start, event) order per parent: stable sort by start, then
+  // stable sort by parent slot (nodes are in event order to begin with)
+  pmp::k_gather_u64<<<blocks_for(nl), 256, 0, s>>>(d_start, lay, nl,
+                                                    0x8000000000000000ull, 0, skey);
+  pmp::k_iota<<<blocks_for(nl), 256, 0, s>>>(ord, nl);
+  if (event_id) {
+    // ties by event id rather than input order: sort by it first (LSD)
+    const long long* d_eid = (const long long*)A.upload(event_id, n);
+    u64* ekey = A.alloc<u64>(nl);
+    u64* ekey2 = A.alloc<u64>(nl);
+    long long* eord = A.alloc<long long>(nl);
+    if (A.err != cudaSuccess) return perr(PM_ERR_CUDA, "pm_layer_tree: alloc");
+    pmp::k_gather_u64<<<blocks_for(nl), 256, 0, s>>>(d_eid, lay, nl,
+                                                      0x8000000000000000ull, 0, ekey);
+    cub::DeviceRadixSort::SortPairs(t, tmp, ekey, ekey2, ord, eord, (int64_t)nl, 0, 64, s);
+    pmp::k_gather_u64<<<blocks_for(nl), 256, 0, s>>>(d_start, lay, nl, 0, 0, skey2);
+    // skey[i] = start of node eord[i] (biased)
+    pmp::k_gather_u64_idx<<<blocks_for(nl), 256, 0, s>>>(skey2, eord, nl,
+                                                          0x8000000000000000ull, skey);
+    cudaMemcpyAsync(ord, eord, nl * sizeof(long long), cudaMemcpyDeviceToDevice, s);
+  }
+  cub::DeviceRadixSort::SortPairs(t, tmp, skey, skey2, ord, ord2, (int64_t)nl, 0, 64, s);
+  pmp::k_gather_parent_key<<<blocks_for(nl), 256, 0, s>>>(d_np, ord2, nl, pkey);
+  cub::DeviceRadixSort::SortPairs(t, tmp, pkey, pkey2, ord2, ord, (int64_t)nl, 0, 32, s);
+  pmp::k_child_off<<<blocks_for(nl + 2), 256, 0, s>>>(pkey2, nl, off);
+  // depth (pointer jumping) and nodes grouped by depth
+  pmp::k_depth_init<<<blocks_for(nl), 256, 0, s>>>(d_np, nl, jump[0], depth[0]);
+  int cur = 0;
+  for (long long span = 1; span < 2 * nl; span *= 2) {
+    pmp::k_depth_step<<<blocks_for(nl), 256, 0, s>>>(jump[cur], depth[cur], nl,
+                                                     jump[cur ^ 1], depth[cur ^ 1]);
+    cur ^= 1;
+  }
+  pmp::k_depth_final<<<blocks_for(nl), 256, 0, s>>>(jump[cur], nl, depth[cur]);
+  pmp::k_iota<<<blocks_for(nl), 256, 0, s>>>(nodes, nl);
+  cub::DeviceRadixSort::SortPairs(t, tmp, depth[cur], sdepth, nodes, by_depth, (int64_t)nl, 0, 32, s);
+  cub::DeviceReduce::Max(t, tmp, depth[cur], dmax, (int64_t)nl, s);
+  int maxd = 0;
+  rc = download(&maxd, dmax, 1, s);
+  if (rc == PM_SUCCESS) rc = download(node_parent, (const int64_t*)d_np, nl, s);
+  if (rc == PM_SUCCESS) rc = download(child_order, (const int64_t*)ord, nl, s);
+  if (rc == PM_SUCCESS) rc = download(child_off, (const int64_t*)off, nl + 2, s);
+  if (rc == PM_SUCCESS) rc = sync_check(s, "pm_layer_tree: depth");
+  if (rc != PM_SUCCESS) return rc;
+  if (maxd < 0) return PM_SUCCESS;  // no frame reaches the root: empty walk
+  long long* lvl = A.alloc<long long>(maxd + 2);
+  if (A.err != cudaSuccess) return perr(PM_ERR_CUDA, "pm_layer_tree: alloc");
+  pmp::k_level_off<<<blocks_for(maxd + 2), 256, 0, s>>>(sdepth, nl, maxd, lvl);
+  std::vector<long long> h_lvl(maxd + 2);
+  rc = download(h_lvl.data(), lvl, maxd + 2, s);
+  if (rc == PM_SUCCESS) rc = sync_check(s, "pm_layer_tree: levels");
+  if (rc != PM_SUCCESS) return rc;
+  // subtree sizes bottom-up, pre-order positions top-down
+  for (int d = maxd; d >= 0; --d) {
+    const long long a = h_lvl[d], b = h_lvl[d + 1];
+    if (b > a)
+      pmp::k_subtree_level<<<blocks_for(b - a), 256, 0, s>>>(by_depth + a, b - a,
+                                                              ord, off, size);
+  }
+  const long long m1 = -1;
+  cudaMemcpyAsync(minus1, &m1, sizeof(long long), cudaMemcpyHostToDevice, s);
+  pmp::k_preorder_level<<<1, 32, 0, s>>>(minus1, 1, ord, off, size, pre);
+  for (int d = 0; d < maxd; ++d) {
+    const long long a = h_lvl[d], b = h_lvl[d + 1];
+    if (b > a)
+      pmp::k_preorder_level<<<blocks_for(b - a), 256, 0, s>>>(by_depth + a, b - a,
+                                                               ord, off, size, pre);
+  }
+  // reachable nodes: depth >= 0, i.e. by_depth[h_lvl[0] ..]
+  const long long r0 = h_lvl[0], nr = h_lvl[maxd + 1] - h_lvl[0];
+  pmp::k_scatter_walk<<<blocks_for(nr), 256, 0, s>>>(by_depth + r0, nr, pre, d_walk);
+  rc = download(walk, (const int64_t*)d_walk, nr, s);
+  if (rc != PM_SUCCESS) return rc;
+  if (n_walk) *n_walk = nr;
+  return sync_check(s, "pm_layer_tree");
 }
 
 }  // extern "C"

@@ -118,6 +118,8 @@ int query_occupancy(Occupancy* out) {
     int rc;
     if (o.warps == 12)
       rc = setup_kernel<12>(optin, cap, &o.buckets, &o.smem, &o.per_sm);
+    else if (o.warps == 14)
+      rc = setup_kernel<14>(optin, cap, &o.buckets, &o.smem, &o.per_sm);
     else {
       o.warps = 16;
       rc = setup_kernel<16>(optin, cap, &o.buckets, &o.smem, &o.per_sm);
@@ -240,6 +242,8 @@ int replay_batch_impl(const pm_req_t* reqs, const int64_t* trace_offsets,
       0, trace_order, n_traces, list1, occ.buckets, group_end, n_groups, ready)
   if (occ.warps == 12)
     PM_LAUNCH_MAIN(12);
+  else if (occ.warps == 14)
+    PM_LAUNCH_MAIN(14);
   else
     PM_LAUNCH_MAIN(16);
 #undef PM_LAUNCH_MAIN

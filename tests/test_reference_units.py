@@ -1,8 +1,9 @@
 """The reference's own unit cases for analysis and linking
 (pkg/tests/test_analysis.py:45-248, pkg/tests/test_linking.py:39-190),
 restated against this package's API: same inputs, same expected values.
-Layer tree and markers are host code (CPU tests); operator roots, grouping
-and the three link steps run on the GPU (pm_link / pm_link_roots)."""
+Markers are host code (CPU tests); the layer tree, operator roots,
+grouping and the three link steps run on the GPU (pm_layer_tree / pm_link /
+pm_link_roots)."""
 
 from __future__ import annotations
 
@@ -44,8 +45,10 @@ def mem(ts, addr, nbytes):
                       0, addr=addr, nbytes=nbytes)
 
 
-# ---- layer tree (test_analysis.py:45-104) -------------------------------------
+# ---- layer tree (test_analysis.py:45-104), GPU (pm_layer_tree) ----------------
 
+@pytest.mark.gpu
+@pytest.mark.usefixtures("require_gpu")
 def test_tree_root_with_two_children():
     tree = build_layer_tree([fn("nn.Module: Sequential_0", 0, 100, 1),
                              fn("nn.Module: Linear_0", 10, 20, 2, 1),
@@ -56,6 +59,8 @@ def test_tree_root_with_two_children():
     assert [c.name for c in seq.children] == ["Linear_0", "ReLU_0"]
 
 
+@pytest.mark.gpu
+@pytest.mark.usefixtures("require_gpu")
 def test_tree_non_layer_frame_collapsed():
     tree = build_layer_tree([
         fn("nn.Module: Block_0", 0, 100, 1),
@@ -65,11 +70,15 @@ def test_tree_non_layer_frame_collapsed():
     assert [c.name for c in tree.children[0].children] == ["Linear_0"]
 
 
+@pytest.mark.gpu
+@pytest.mark.usefixtures("require_gpu")
 def test_tree_orphan_attaches_to_root():
     tree = build_layer_tree([fn("nn.Module: Linear_0", 0, 10, 1, 999)])
     assert [c.name for c in tree.children] == ["Linear_0"]
 
 
+@pytest.mark.gpu
+@pytest.mark.usefixtures("require_gpu")
 def test_tree_wrapper_flag():
     tree = build_layer_tree([fn("nn.Module: Sequential_0", 0, 100, 1),
                              fn("nn.Module: Linear_0", 10, 20, 2, 1)])
@@ -77,6 +86,8 @@ def test_tree_wrapper_flag():
     assert not tree.children[0].children[0].is_wrapper
 
 
+@pytest.mark.gpu
+@pytest.mark.usefixtures("require_gpu")
 def test_tree_cycle_detected():
     with pytest.raises(CyclicParentLink):
         build_layer_tree([fn("nn.Module: A_0", 0, 10, 1, 2),
@@ -88,6 +99,8 @@ def test_tree_rejects_wrong_category():
         build_layer_tree([op("aten::add", 0, 1)])
 
 
+@pytest.mark.gpu
+@pytest.mark.usefixtures("require_gpu")
 def test_tree_children_sorted_by_time():
     tree = build_layer_tree([fn("nn.Module: B_0", 50, 10, 2),
                              fn("nn.Module: A_0", 0, 10, 1)])
