@@ -6,6 +6,7 @@
 
 #include "peakmem_b200.h"
 #include "replay_device.cuh"
+#include "replay_narrow.cuh"
 
 // ---------------------------------------------------------------------------
 // Host side of the C ABI.
@@ -29,7 +30,8 @@ int cuda_fail(cudaError_t e, const char* where) {
   return fail(PM_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
 }
 
-constexpr int kWarps = 12;
+constexpr int kWarps = 12;        // wide main kernel (PM_REPLAY_WIDE=1)
+constexpr int kNarrowWarps = 16;  // narrow main kernel
 constexpr size_t kBucket_host = 32;  // warps (traces in flight) per CTA, 1 CTA / SM
 constexpr int kRetryWarps = 1;
 constexpr int kMaxRetryWarps = 64;
@@ -66,6 +68,7 @@ Layout layout_for(int64_t total_events, int64_t max_trace_events,
 struct Occupancy {
   int sms = 0, per_sm = 0, buckets = 0, warps = 0;
   size_t smem = 0;
+  bool narrow = true;  // main pass: replay_narrow_kernel (else the wide kernel)
   int per_sm1 = 0;  // tier-1 retry kernel
   size_t smem1 = 0;
   int nbmax2 = 0;   // tier-2: one warp with a shared-memory directory
@@ -92,6 +95,24 @@ int setup_kernel(int optin, int cap, int* buckets, size_t* smem, int* per_sm) {
   return PM_SUCCESS;
 }
 
+template <int W>
+int setup_narrow(int optin, int cap, int* buckets, size_t* smem, int* per_sm) {
+  int b = (int)(((size_t)optin - (size_t)W * 32 * 16 - 256) / (kBucket_host * 16));
+  if (cap > 0 && cap < b) b = cap;
+  if (b < 2 * W) b = 2 * W;
+  *buckets = b;
+  *smem = pmn::smem_cta_bytes(b, W);
+  cudaError_t e = cudaFuncSetAttribute(
+      pmn::replay_narrow_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      (int)*smem);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute narrow");
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+      per_sm, pmn::replay_narrow_kernel<W>, W * 32, *smem);
+  if (e != cudaSuccess) return cuda_fail(e, "occupancy narrow");
+  if (*per_sm < 1) return fail(PM_ERR_CUDA, "narrow replay kernel cannot be resident");
+  return PM_SUCCESS;
+}
+
 // Main pass: one CTA of `warps` warps per SM sharing a bucket pool sized to
 // the remaining shared memory (PM_POOL_BUCKETS caps it, PM_REPLAY_WARPS picks
 // 12 or 16 warps; 12 measured faster on C3).  Tier 1: 8 warps x 32 dedicated buckets.
@@ -113,10 +134,21 @@ int query_occupancy(Occupancy* out) {
     if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceGetAttribute");
     int cap = 0;
     if (const char* env = getenv("PM_POOL_BUCKETS")) cap = atoi(env);
-    o.warps = kWarps;
+    const char* wide = getenv("PM_REPLAY_WIDE");
+    o.narrow = !(wide && atoi(wide) != 0);
+    o.warps = o.narrow ? kNarrowWarps : kWarps;
     if (const char* env = getenv("PM_REPLAY_WARPS")) o.warps = atoi(env);
     int rc;
-    if (o.warps == 12)
+    if (o.narrow) {
+      if (o.warps == 12)
+        rc = setup_narrow<12>(optin, cap, &o.buckets, &o.smem, &o.per_sm);
+      else if (o.warps == 20)
+        rc = setup_narrow<20>(optin, cap, &o.buckets, &o.smem, &o.per_sm);
+      else {
+        o.warps = 16;
+        rc = setup_narrow<16>(optin, cap, &o.buckets, &o.smem, &o.per_sm);
+      }
+    } else if (o.warps == 12)
       rc = setup_kernel<12>(optin, cap, &o.buckets, &o.smem, &o.per_sm);
     else if (o.warps == 14)
       rc = setup_kernel<14>(optin, cap, &o.buckets, &o.smem, &o.per_sm);
@@ -236,17 +268,30 @@ int replay_batch_impl(const pm_req_t* reqs, const int64_t* trace_offsets,
     const long long g = atoll(cap);
     if (g > 0 && g < grid) grid = g;
   }
+#define PM_LAUNCH_NARROW(W)                                                   \
+  pmn::replay_narrow_kernel<W><<<(unsigned)grid, W * 32, occ.smem, stream>>>( \
+      reqs, trace_offsets, cfgs, cfg_of_trace, results, timeline,             \
+      reinterpret_cast<pmb::u32*>(recs), ctl, trace_order, n_traces, list1,   \
+      occ.buckets, group_end, n_groups, ready)
 #define PM_LAUNCH_MAIN(W)                                                     \
   pmb::replay_smem_kernel<W><<<(unsigned)grid, W * 32, occ.smem, stream>>>(  \
       reqs, trace_offsets, cfgs, cfg_of_trace, results, timeline, recs, ctl, \
       0, trace_order, n_traces, list1, occ.buckets, group_end, n_groups, ready)
-  if (occ.warps == 12)
+  if (occ.narrow) {
+    if (occ.warps == 12)
+      PM_LAUNCH_NARROW(12);
+    else if (occ.warps == 20)
+      PM_LAUNCH_NARROW(20);
+    else
+      PM_LAUNCH_NARROW(16);
+  } else if (occ.warps == 12)
     PM_LAUNCH_MAIN(12);
   else if (occ.warps == 14)
     PM_LAUNCH_MAIN(14);
   else
     PM_LAUNCH_MAIN(16);
 #undef PM_LAUNCH_MAIN
+#undef PM_LAUNCH_NARROW
   e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "replay_smem_kernel launch");
   // tier 1: dedicated 32-bucket pools (grid sized for the worst case; idle

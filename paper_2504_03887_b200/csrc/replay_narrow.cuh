@@ -1,0 +1,808 @@
+// Narrow-encoded replay: the main pass of pm_replay_batch (sm_100a).
+//
+// Same state machine as replay_device.cuh (peakmem.allocator.AllocatorState,
+// reference pkg/src/peakmem/allocator.py:155-393), same data structures, but
+// every block size and address is held in *allocator units* as a 32-bit
+// value.  Every block size and address the reference can produce is a
+// multiple of
+//
+//     u = 2^s,  s = min(ctz(alignment), ctz(k_small_buffer),
+//                       ctz(k_large_buffer), ctz(k_round_large))
+//
+// (rounded requests are multiples of the power-of-two alignment,
+// allocator.py:79-83; segments are k_small_buffer, k_large_buffer or a
+// multiple of k_round_large, :86-92; addresses are sums of both), so
+// size_u = size >> s and addr_u = addr >> s are exact.  With that:
+//
+//  * a free block is ONE 64-bit word ka = size_u << 32 | addr_u, and the
+//    best-fit order (size, addr) (allocator.py:203-221) is plain unsigned
+//    order of ka: directory search, bucket split ranks and the argmin are
+//    single 64-bit compares instead of (key, addr) pairs;
+//  * a pool entry is 16 B (ka + links) instead of 24 B, so the CTA-shared
+//    shared-memory pool holds 1.5x the entries and more traces fit per SM;
+//  * an allocated-block record is 16 B (addr_u, size_u, left ref, right
+//    ref): one 128-bit gather per request instead of four 64-bit loads.
+//
+// The encoding covers one stream (stream 0) and next_base_u < 2^32 - 1
+// (2 TiB of segments ever reserved at u = 512).  A trace that leaves it
+// (another stream, a larger block or address space) stops with
+// PM_POOL_OVERFLOW and is replayed from the start by the wide tiers
+// (replay_device.cuh), exactly like a trace whose free blocks outgrow the
+// shared pool; results are bit-identical either way.
+#pragma once
+
+#include "replay_device.cuh"
+
+namespace pmn {
+
+using pmb::kBucket;
+using pmb::kFreeTag;
+using pmb::kFull;
+using pmb::kHalf;
+using pmb::kNone;
+using pmb::is_free_ref;
+using pmb::lanemask_lt;
+using pmb::u32;
+using pmb::u64;
+
+constexpr u32 kFreedU = 0xFFFFFFFFu;  // record size of a freed handle
+constexpr u32 kMaxU = 0xFFFFFFFEu;    // sizes / addresses stay below this
+
+__device__ __forceinline__ u32 hi(u64 x) { return (u32)(x >> 32); }
+__device__ __forceinline__ u32 lo(u64 x) { return (u32)x; }
+__device__ __forceinline__ u64 pk(u32 h, u32 l) {
+  return ((u64)h << 32) | (u64)l;
+}
+
+// Free-block entries: ka = size_u << 32 | addr_u, ln = left | right << 32
+// (neighbour handles or kNone).
+struct NPool {
+  u64* ka;
+  u64* ln;
+};
+
+// Allocated-block records, 16 B per handle: x addr_u, y size_u (0 never
+// allocated, kFreedU freed), z left ref, w right ref.
+struct NRecs {
+  u32* base;
+  __device__ __forceinline__ u32* word(u32 h, int w) const {
+    return base + 4 * (size_t)h + w;
+  }
+};
+
+// Directory in registers: lane d holds bucket position d -- its lower bound
+// (packed ka), physical bucket and entry count.
+struct NDir {
+  u64 db;
+  int dp, dc;
+  int nb;
+  int lane;
+  unsigned* cta_used;  // CTA-shared bitmap of physical buckets in use
+  int cta_words, cta_buckets;
+
+  __device__ __forceinline__ void init(int lane_) {
+    db = ~0ull;
+    dp = -1;
+    dc = 0;
+    nb = 0;
+    lane = lane_;
+  }
+  // last position whose bound <= x (nb > 0: position 0's bound is 0)
+  __device__ __forceinline__ int find(u64 x) const {
+    return 31 - __clz(__ballot_sync(kFull, db <= x));
+  }
+  __device__ __forceinline__ int phys(int d) const {
+    return __shfl_sync(kFull, dp, d);
+  }
+  __device__ __forceinline__ int count(int d) const {
+    return __shfl_sync(kFull, dc, d);
+  }
+  __device__ __forceinline__ void add_count(int d, int delta) {
+    if (lane == d) dc += delta;
+  }
+  __device__ __forceinline__ void set_count(int d, int c) {
+    if (lane == d) dc = c;
+  }
+  __device__ __forceinline__ int pos_of_phys(int p) const {
+    return __ffs(__ballot_sync(kFull, dp == p)) - 1;
+  }
+  __device__ __forceinline__ int mergeable() const {
+    const int cn = __shfl_down_sync(kFull, dc, 1);
+    const unsigned m =
+        __ballot_sync(kFull, lane < nb - 1 && dc + cn <= kBucket);
+    return m ? __ffs(m) - 1 : -1;
+  }
+  __device__ __forceinline__ void insert(int d, u64 b, int p, int c) {
+    const u64 ub = __shfl_up_sync(kFull, db, 1);
+    const int up = __shfl_up_sync(kFull, dp, 1);
+    const int uc = __shfl_up_sync(kFull, dc, 1);
+    if (lane > d) {
+      db = ub;
+      dp = up;
+      dc = uc;
+    } else if (lane == d) {
+      db = b;
+      dp = p;
+      dc = c;
+    }
+    nb += 1;
+  }
+  __device__ __forceinline__ void erase(int d) {
+    u64 nbd = __shfl_down_sync(kFull, db, 1);
+    int np = __shfl_down_sync(kFull, dp, 1);
+    int nc = __shfl_down_sync(kFull, dc, 1);
+    if (lane == 31) {
+      nbd = ~0ull;
+      np = -1;
+      nc = 0;
+    }
+    if (lane >= d) {
+      db = nbd;
+      dp = np;
+      dc = nc;
+    }
+    nb -= 1;
+    if (d == 0 && lane == 0) db = 0;
+  }
+  __device__ __forceinline__ int alloc_phys() {
+    int p = -1;
+    if (lane == 0) {
+      for (int w = 0; w < cta_words && p < 0; ++w) {
+        unsigned v = cta_used[w];
+        while (v != 0xffffffffu) {
+          const int b = __ffs(~v) - 1;
+          const unsigned old = atomicOr(&cta_used[w], 1u << b);
+          if (!(old & (1u << b))) {
+            p = w * 32 + b;
+            break;
+          }
+          v = old | (1u << b);
+        }
+      }
+      if (p >= cta_buckets) p = -1;
+    }
+    return __shfl_sync(kFull, p, 0);
+  }
+  __device__ __forceinline__ void free_phys(int p) {
+    if (lane == 0) atomicAnd(&cta_used[p >> 5], ~(1u << (p & 31)));
+  }
+  __device__ __forceinline__ void release_all() {
+    if (lane < nb) atomicAnd(&cta_used[dp >> 5], ~(1u << (dp & 31)));
+    nb = 0;
+  }
+  __device__ __forceinline__ bool full() const { return nb >= 32; }
+};
+
+struct NCtx {
+  long long reserved, allocated, peak_reserved, peak_allocated;
+  u32 next_base;  // units
+  int F, maxF, nseg, nseg_peak;
+};
+
+// ---- record refs (global store + staged mirror) ---------------------------
+
+__device__ __forceinline__ void set_link(const NRecs& rec, uint4* st, int hcmp,
+                                         int lane, u32 g, int right, u32 val) {
+  if (lane == 0) *rec.word(g, 2 + right) = val;
+  if (hcmp == (int)g) {
+    if (right)
+      st[lane].w = val;
+    else
+      st[lane].z = val;
+  }
+}
+
+__device__ __forceinline__ void relink(const NRecs& rec, uint4* st, int hcmp,
+                                       int lane, u64 l, int id) {
+  const u32 L = lo(l), R = hi(l);
+  if (L != kNone) set_link(rec, st, hcmp, lane, L, 1, kFreeTag | (u32)id);
+  if (R != kNone) set_link(rec, st, hcmp, lane, R, 0, kFreeTag | (u32)id);
+}
+
+__device__ __forceinline__ void relink_lanes(const NRecs& rec, uint4* st,
+                                             int hcmp, int lane, bool moved,
+                                             u64 links, int dst) {
+  const u32 L = lo(links), R = hi(links);
+  const u32 val = kFreeTag | (u32)dst;
+  if (moved) {
+    if (L != kNone) *rec.word(L, 3) = val;
+    if (R != kNone) *rec.word(R, 2) = val;
+  }
+  unsigned m = __ballot_sync(kFull, moved);
+  while (m) {
+    const int src = __ffs(m) - 1;
+    m &= m - 1;
+    const u32 gl = __shfl_sync(kFull, L, src);
+    const u32 gr = __shfl_sync(kFull, R, src);
+    const u32 v = __shfl_sync(kFull, val, src);
+    if (gl != kNone && hcmp == (int)gl) st[lane].w = v;
+    if (gr != kNone && hcmp == (int)gr) st[lane].z = v;
+  }
+  __syncwarp();
+}
+
+// argmin of distinct packed values over the valid lanes (-1 if none)
+__device__ __forceinline__ int argmin_pk(bool valid, u64 x) {
+  const unsigned any = __ballot_sync(kFull, valid);
+  if (!any) return -1;
+  if ((any & (any - 1)) == 0) return __ffs(any) - 1;
+  const u32 mh = __reduce_min_sync(kFull, valid ? hi(x) : 0xffffffffu);
+  const bool c = valid && hi(x) == mh;
+  const unsigned bm = __ballot_sync(kFull, c);
+  if ((bm & (bm - 1)) == 0) return __ffs(bm) - 1;
+  const u32 ml = __reduce_min_sync(kFull, c ? lo(x) : 0xffffffffu);
+  return __ffs(__ballot_sync(kFull, c && lo(x) == ml)) - 1;
+}
+
+// ---- bucket maintenance -----------------------------------------------------
+
+__device__ __forceinline__ bool try_merge(const NPool& P, NDir& dir,
+                                          const NRecs& rec, uint4* st,
+                                          int hcmp, int lane) {
+  const int e = dir.mergeable();
+  if (e < 0) return false;
+  const int pa = dir.phys(e), pb = dir.phys(e + 1);
+  const int na = dir.count(e), nbb = dir.count(e + 1);
+  const bool mv = lane < nbb;
+  u64 ka = 0, l = 0;
+  const int src = pb * kBucket + lane, dst = pa * kBucket + na + lane;
+  if (mv) {
+    ka = P.ka[src];
+    l = P.ln[src];
+  }
+  __syncwarp();
+  if (mv) {
+    P.ka[dst] = ka;
+    P.ln[dst] = l;
+  }
+  __syncwarp();
+  relink_lanes(rec, st, hcmp, lane, mv, l, dst);
+  dir.set_count(e, na + nbb);
+  dir.erase(e + 1);
+  dir.free_phys(pb);
+  return true;
+}
+
+// Split the full bucket at position d into halves by ka rank.  False if no
+// bucket can be had and nothing merges (overflow).
+__device__ __forceinline__ bool split_bucket(const NPool& P, NDir& dir, int d,
+                                             const NRecs& rec, uint4* st,
+                                             int hcmp, int lane) {
+  const int q = dir.full() ? -1 : dir.alloc_phys();
+  if (q < 0) return try_merge(P, dir, rec, st, hcmp, lane);
+  const int p = dir.phys(d);
+  const int base = p * kBucket;
+  const u64 ka = P.ka[base + lane];
+  const u64 l = P.ln[base + lane];
+  int rank = 0;
+#pragma unroll 8
+  for (int j = 0; j < kBucket; ++j)
+    rank += __shfl_sync(kFull, ka, j) < ka ? 1 : 0;
+  const bool up = rank >= kHalf;
+  const unsigned holes = __ballot_sync(kFull, up && lane < kHalf);
+  const unsigned movers = __ballot_sync(kFull, !up && lane >= kHalf);
+  int dst;
+  if (up) {
+    dst = q * kBucket + rank - kHalf;
+  } else if (lane >= kHalf) {
+    const int r = __popc(movers & lanemask_lt());
+    dst = base + (int)__fns(holes, 0, r + 1);
+  } else {
+    dst = base + lane;
+  }
+  const int bl = __ffs(__ballot_sync(kFull, rank == kHalf)) - 1;
+  const u64 bound = __shfl_sync(kFull, ka, bl);
+  __syncwarp();
+  P.ka[dst] = ka;
+  P.ln[dst] = l;
+  __syncwarp();
+  dir.set_count(d, kHalf);
+  dir.insert(d + 1, bound, q, kHalf);
+  relink_lanes(rec, st, hcmp, lane, dst != base + lane, l, dst);
+  return true;
+}
+
+__device__ __forceinline__ int pool_insert(const NPool& P, NDir& dir, NCtx& c,
+                                           u64 ka, u64 links, const NRecs& rec,
+                                           uint4* st, int hcmp, int lane) {
+  if (dir.nb == 0) {
+    const int q = dir.alloc_phys();
+    if (q < 0) return -1;
+    dir.insert(0, 0ull, q, 0);
+  }
+  int d = dir.find(ka);
+  int cnt = dir.count(d);
+  while (cnt >= kBucket) {
+    if (!split_bucket(P, dir, d, rec, st, hcmp, lane)) return -1;
+    d = dir.find(ka);
+    cnt = dir.count(d);
+  }
+  const int id = dir.phys(d) * kBucket + cnt;
+  __syncwarp();
+  P.ka[id] = ka;
+  P.ln[id] = links;
+  dir.add_count(d, 1);
+  c.F += 1;
+  return id;
+}
+
+__device__ __forceinline__ int pool_remove(const NPool& P, NDir& dir, NCtx& c,
+                                           int id, const NRecs& rec, uint4* st,
+                                           int hcmp, int lane) {
+  const int p = id / kBucket;
+  const int d = dir.pos_of_phys(p);
+  const int last = dir.count(d) - 1;
+  const int lid = p * kBucket + last;
+  int moved = -1;
+  if (lid != id) {
+    const u64 lka = P.ka[lid], ll = P.ln[lid];
+    __syncwarp();
+    P.ka[id] = lka;
+    P.ln[id] = ll;
+    relink(rec, st, hcmp, lane, ll, id);
+    moved = lid;
+  }
+  dir.add_count(d, -1);
+  c.F -= 1;
+  if (last == 0 && dir.nb > 1) {
+    dir.erase(d);
+    dir.free_phys(p);
+  }
+  return moved;
+}
+
+__device__ __forceinline__ int pool_upsert(const NPool& P, NDir& dir, NCtx& c,
+                                           int id, u64 ka, u64 links,
+                                           const NRecs& rec, uint4* st,
+                                           int hcmp, int lane) {
+  if (id >= 0) {
+    const int d = dir.find(ka);
+    if (dir.phys(d) == id / kBucket) {
+      __syncwarp();
+      P.ka[id] = ka;
+      P.ln[id] = links;
+      return id;
+    }
+    pool_remove(P, dir, c, id, rec, st, hcmp, lane);
+  }
+  return pool_insert(P, dir, c, ka, links, rec, st, hcmp, lane);
+}
+
+// Best fit (allocator.py:203-221): argmin ka over entries
+// with ru <= size_u and size_u - ru < span (span > 2^32: no bound).
+__device__ __forceinline__ int best_fit(const NPool& P, const NDir& dir,
+                                        u32 ru, u64 span, int lane) {
+  if (dir.nb == 0) return -1;
+  const int d = dir.find((u64)ru << 32);
+  {
+    const int p = dir.phys(d);
+    const int id = p * kBucket + lane;
+    const bool in = lane < dir.count(d);
+    const u64 ka = in ? P.ka[id] : ~0ull;
+    const bool el = in && (u64)hi(ka) - (u64)ru < span;
+    const int w = argmin_pk(el, ka);
+    if (w >= 0) return p * kBucket + w;
+  }
+  if (d + 1 < dir.nb) {
+    // every entry of the next bucket is larger: its minimum is the only
+    // remaining candidate
+    const int p = dir.phys(d + 1);
+    const int id = p * kBucket + lane;
+    const bool in = lane < dir.count(d + 1);
+    const u64 ka = in ? P.ka[id] : ~0ull;
+    const int w = argmin_pk(in, ka);
+    if (w >= 0) {
+      const u64 kw = __shfl_sync(kFull, ka, w);
+      if ((u64)hi(kw) - (u64)ru < span) return p * kBucket + w;
+    }
+  }
+  return -1;
+}
+
+// Wholly-free segment (entry with no allocated neighbour) of largest size_u
+// > thr (thr < 0: any), ties lowest addr; -1 if none.
+__device__ __forceinline__ int find_release_candidate(const NPool& P,
+                                                      const NDir& dir,
+                                                      long long thr, int lane) {
+  u64 best = ~0ull;
+  int bid = -1;
+  for (int d = 0; d < dir.nb; ++d) {
+    const int p = dir.phys(d);
+    const int id = p * kBucket + lane;
+    if (lane < dir.count(d) && P.ln[id] == ~0ull) {
+      const u64 ka = P.ka[id];
+      if ((long long)hi(ka) > thr) {
+        const u64 key = pk(0xFFFFFFFFu - hi(ka), lo(ka));
+        if (key < best) {
+          best = key;
+          bid = id;
+        }
+      }
+    }
+  }
+  const int w = argmin_pk(bid >= 0, best);
+  return w < 0 ? -1 : __shfl_sync(kFull, bid, w);
+}
+
+struct NCfg {
+  const pm_cfg_t* cp;
+  u64 amask;         // alignment - 1 (bytes)
+  int s;             // unit shift
+  u64 span;          // best-fit window in units (> 2^32: unbounded)
+  u32 split_lim;     // splittable iff size_u <= split_lim
+  long long rel_thr; // stage-1 release threshold in units (max_split)
+  bool has_split;
+};
+
+__device__ __forceinline__ void make_room(const NPool& P, NDir& dir, NCtx& c,
+                                          long long seg, const NCfg& cf,
+                                          const NRecs& rec, uint4* st,
+                                          int hcmp, int lane) {
+  const long long capacity = cf.cp->device_capacity;
+  int stage = cf.has_split ? 1 : 2;
+  if (stage == 2 && c.reserved + seg <= capacity) return;
+  for (;;) {
+    if (stage == 1 && c.reserved + seg <= capacity) break;
+    const int id = find_release_candidate(P, dir, stage == 1 ? cf.rel_thr : -1,
+                                          lane);
+    if (id < 0) {
+      if (stage == 2 || c.reserved + seg <= capacity) break;
+      stage = 2;
+      continue;
+    }
+    const long long sz = (long long)hi(P.ka[id]) << cf.s;
+    pool_remove(P, dir, c, id, rec, st, hcmp, lane);
+    c.reserved -= sz;
+    c.nseg -= 1;
+  }
+}
+
+__device__ __forceinline__ int ctz64(long long v) {
+  return __ffsll(v) - 1;
+}
+
+// ---- one trace ---------------------------------------------------------------
+
+__device__ __forceinline__ void replay_trace(
+    int tr, const pm_req_t* __restrict__ reqs, const int64_t* __restrict__ offs,
+    const pm_cfg_t* __restrict__ cfgs, const int32_t* __restrict__ cfg_of,
+    pm_result_t* __restrict__ results, int64_t* __restrict__ timeline,
+    u32* rec_base, const NPool& P, NDir& dir, uint4* st, int lane) {
+  const long long e0 = offs[tr];
+  const long long n = offs[tr + 1] - e0;
+  const pm_cfg_t* cp = cfgs + (cfg_of ? cfg_of[tr] : 0);
+  NCfg cf;
+  cf.cp = cp;
+  cf.amask = (u64)cp->alignment - 1;
+  {
+    int s = ctz64(cp->alignment);
+    s = min(s, ctz64(cp->k_small_buffer));
+    s = min(s, ctz64(cp->k_large_buffer));
+    s = min(s, ctz64(cp->k_round_large));
+    cf.s = s;
+  }
+  const int s = cf.s;
+  const long long t = cp->max_split_size;
+  cf.has_split = t >= 0;
+  if (t >= 0) {
+    cf.span = ((u64)t + ((1ull << s) - 1)) >> s;  // ceil(t / u)
+    const u64 fl = (u64)t >> s;
+    cf.split_lim = fl > 0xFFFFFFFFull ? 0xFFFFFFFFu : (u32)fl;
+    cf.rel_thr = (long long)fl;
+  } else {
+    cf.span = 1ull << 33;
+    cf.split_lim = 0xFFFFFFFFu;
+    cf.rel_thr = -1;
+  }
+  const u64 amask = cf.amask;
+  // largest request the encoding takes: rounded size_u <= kMaxU (units
+  // above 2^24 B are left to the wide tiers altogether)
+  const u64 size_cap = s > 24 ? 0ull : ((u64)kMaxU << s) - amask;
+
+  NRecs rec;
+  rec.base = rec_base + 4 * (size_t)e0;
+  {
+    uint4* r4 = reinterpret_cast<uint4*>(rec.base);
+    for (long long i = lane; i < n; i += 32) r4[i] = make_uint4(0, 0, 0, 0);
+  }
+  dir.init(lane);
+  __syncwarp();
+
+  NCtx c;
+  c.reserved = c.allocated = c.peak_reserved = c.peak_allocated = 0;
+  c.next_base = 0;
+  c.F = c.maxF = c.nseg = c.nseg_peak = 0;
+  int status = PM_OK;
+  long long stop = -1;
+
+  const ulonglong2* rq = reinterpret_cast<const ulonglong2*>(reqs + e0);
+  ulonglong2 nxt = make_ulonglong2(0ull, 0xFFFFFFFFull);
+  if (lane < n) nxt = __ldg(rq + lane);
+
+  for (long long cbase = 0; cbase < n; cbase += 32) {
+    const ulonglong2 ev = nxt;
+    if (cbase + 32 + lane < n) nxt = __ldg(rq + cbase + 32 + lane);
+    const long long my_size = (long long)ev.x;
+    const int my_h = (int)lo(ev.y);
+    const unsigned my_ks = hi(ev.y);
+    const bool my_valid = cbase + lane < n;
+    const bool hok = my_valid && my_h >= 0 && (long long)my_h < n;
+    uint4 r = make_uint4(0, 0, 0, 0);
+    if (hok) r = *reinterpret_cast<const uint4*>(rec.word((u32)my_h, 0));
+    st[lane] = r;
+    const int hcmp = hok ? my_h : -1;
+    __syncwarp();
+
+    const int cnt = (int)((n - cbase) < 32 ? (n - cbase) : 32);
+    long long tl_r = 0, tl_a = 0;
+    int done = cnt;
+    for (int j = 0; j < cnt; ++j) {
+      const long long size = __shfl_sync(kFull, my_size, j);
+      const int hj = __shfl_sync(kFull, my_h, j);
+      const unsigned ks = __shfl_sync(kFull, my_ks, j);
+      const unsigned kind = ks & 3u;
+      const unsigned m = __ballot_sync(kFull, hcmp == hj) & ((1u << j) - 1u);
+      const int src = m ? 31 - __clz(m) : j;
+      int sts = PM_OK;
+      if (kind >= PM_KIND_UNKNOWN) {
+        sts = kind == PM_KIND_UNKNOWN ? PM_UNKNOWN_KIND : PM_MISSING_FIELD;
+      } else if ((unsigned)hj >= (unsigned long long)n) {
+        sts = PM_BAD_HANDLE;
+      } else {
+        const uint4 rj = st[src];
+        int rm_id = -1;
+        bool up = false;
+        int up_id = -1;
+        u64 up_ka = 0, up_l = 0;
+        u32 f1 = kNone, f2 = kNone;
+        int both_pid = -1;
+        u32 both_S = 0, both_rS = 0, both_rR = kNone;
+        const bool is_alloc = kind == PM_KIND_ALLOC;
+        bool split_out = false;
+        u32 out_a = 0, out_s = 0, out_L = kNone, out_R = kNone;
+        if (is_alloc) {
+          if (rj.y != 0) {
+            sts = PM_DUPLICATE_HANDLE;
+          } else if (size <= 0) {
+            sts = PM_ZERO_SIZE;
+          } else if ((ks >> 2) != 0u || (u64)size > size_cap) {
+            sts = PM_POOL_OVERFLOW;  // outside the encoding: wide tiers
+          } else {
+            const u32 ru = (u32)((((u64)size + amask) & ~amask) >> s);
+            const int id = best_fit(P, dir, ru, cf.span, lane);
+            if (id >= 0) {
+              // hit: _take (allocator.py:234-242), _split (:223-232)
+              const u64 KA = P.ka[id];
+              const u64 Lk = P.ln[id];
+              const u32 Lf = lo(Lk), Rf = hi(Lk);
+              const u32 S = hi(KA), A = lo(KA);
+              out_a = A;
+              out_L = Lf;
+              f1 = Lf;
+              if (S <= cf.split_lim && S > ru) {
+                up = true;
+                up_id = id;
+                up_ka = pk(S - ru, A + ru);
+                up_l = pmb::mk_links(kNone, Rf);  // left (hj) set below
+                out_s = ru;
+                split_out = true;
+              } else {
+                rm_id = id;
+                out_s = S;
+                out_R = Rf;
+                f2 = Rf;
+              }
+            } else {
+              // miss: new segment (allocator.py:278-288, 244-250)
+              pmb::Cfg wc;
+              wc.cp = cp;
+              const long long seg =
+                  pmb::segment_size_for((long long)ru << s, wc);
+              const long long capacity = cp->device_capacity;
+              if (capacity >= 0 && c.reserved + seg > capacity) {
+                make_room(P, dir, c, seg, cf, rec, st, hcmp, lane);
+                if (c.reserved + seg > capacity) sts = PM_OOM;
+              }
+              const u64 seg_u = (u64)seg >> s;
+              if (sts == PM_OK && (u64)c.next_base + seg_u > kMaxU)
+                sts = PM_POOL_OVERFLOW;
+              if (sts == PM_OK) {
+                const u32 A = c.next_base;
+                c.next_base += (u32)seg_u;
+                c.reserved += seg;
+                c.nseg += 1;
+                c.nseg_peak = max(c.nseg_peak, c.nseg);
+                out_a = A;
+                if ((u32)seg_u <= cf.split_lim && (u32)seg_u > ru) {
+                  up = true;
+                  up_ka = pk((u32)seg_u - ru, A + ru);
+                  up_l = pmb::mk_links(kNone, kNone);
+                  out_s = ru;
+                  split_out = true;
+                } else {
+                  out_s = (u32)seg_u;
+                }
+              }
+            }
+          }
+        } else {
+          // free (allocator.py:294-320): double free before unknown handle
+          if (rj.y == kFreedU) {
+            sts = PM_DOUBLE_FREE;
+          } else if (rj.y == 0) {
+            sts = PM_UNKNOWN_HANDLE;
+          } else {
+            const u32 A = rj.x, S = rj.y, L = rj.z, R = rj.w;
+            c.allocated -= (long long)S << s;
+            const bool lf = is_free_ref(L), rf = is_free_ref(R);
+            up = true;
+            if (!lf && !rf) {
+              up_ka = pk(S, A);
+              up_l = pmb::mk_links(L, R);
+            } else if (lf && !rf) {
+              const int pid = (int)(L & ~kFreeTag);
+              up_id = pid;
+              up_ka = P.ka[pid] + ((u64)S << 32);
+              up_l = pmb::mk_links(lo(P.ln[pid]), R);
+            } else if (!lf && rf) {
+              const int rid = (int)(R & ~kFreeTag);
+              up_id = rid;
+              up_ka = pk(hi(P.ka[rid]) + S, A);
+              up_l = pmb::mk_links(L, hi(P.ln[rid]));
+            } else {
+              const int rid = (int)(R & ~kFreeTag);
+              both_pid = (int)(L & ~kFreeTag);
+              both_rS = hi(P.ka[rid]);
+              both_rR = hi(P.ln[rid]);
+              both_S = S;
+              rm_id = rid;
+            }
+          }
+        }
+        if (sts == PM_OK) {
+          if (rm_id >= 0) {
+            const int moved = pool_remove(P, dir, c, rm_id, rec, st, hcmp, lane);
+            if (both_pid >= 0) {
+              const int pid = moved == both_pid ? rm_id : both_pid;
+              up_id = pid;
+              up_ka = P.ka[pid] + ((u64)(both_S + both_rS) << 32);
+              up_l = pmb::mk_links(lo(P.ln[pid]), both_rR);
+            }
+          }
+          if (up) {
+            // a split remainder's left neighbour is hj itself: its record
+            // is written whole below, so only the stored entry names it
+            const u64 links = split_out ? (up_l & 0xFFFFFFFF00000000ull) | (u64)(u32)hj
+                                        : up_l;
+            const int nid = pool_upsert(P, dir, c, up_id, up_ka, links, rec, st,
+                                        hcmp, lane);
+            if (nid < 0) {
+              sts = PM_POOL_OVERFLOW;
+            } else {
+              relink(rec, st, hcmp, lane, up_l, nid);
+              if (split_out) out_R = kFreeTag | (u32)nid;
+            }
+          }
+        }
+        if (sts == PM_OK) {
+          if (f2 != kNone) set_link(rec, st, hcmp, lane, f2, 0, (u32)hj);
+          if (f1 != kNone) set_link(rec, st, hcmp, lane, f1, 1, (u32)hj);
+          c.maxF = max(c.maxF, c.F);
+          __syncwarp();
+          if (is_alloc) {
+            c.allocated += (long long)out_s << s;
+            c.peak_reserved = max(c.peak_reserved, c.reserved);
+            c.peak_allocated = max(c.peak_allocated, c.allocated);
+            if (lane == j) {
+              const uint4 o = make_uint4(out_a, out_s, out_L, out_R);
+              st[j] = o;
+              *reinterpret_cast<uint4*>(rec.word((u32)hj, 0)) = o;
+            }
+          } else if (lane == j) {
+            st[j].y = kFreedU;
+            *rec.word((u32)hj, 1) = kFreedU;
+          }
+        }
+      }
+      if (sts != PM_OK) {
+        status = sts;
+        stop = cbase + j;
+        done = j;
+        break;
+      }
+      if (lane == j) {
+        tl_r = c.reserved;
+        tl_a = c.allocated;
+      }
+      __syncwarp();
+    }
+    if (timeline != nullptr && lane < done) {
+      const long long gi = e0 + cbase + lane;
+      reinterpret_cast<longlong2*>(timeline)[gi] = make_longlong2(tl_r, tl_a);
+    }
+    __syncwarp();
+    if (status != PM_OK) break;
+  }
+
+  dir.release_all();
+  if (lane == 0) {
+    pm_result_t res;
+    res.peak_reserved = c.peak_reserved;
+    res.peak_allocated = c.peak_allocated;
+    res.final_reserved = c.reserved;
+    res.final_allocated = c.allocated;
+    res.stop_index = stop;
+    res.n_events_replayed =
+        status == PM_OK ? n : (status == PM_OOM ? stop + 1 : stop);
+    res.status = status;
+    res.n_segments_final = c.nseg;
+    res.n_segments_peak = c.nseg_peak;
+    res.max_free_blocks = c.maxF;
+    results[tr] = res;
+  }
+}
+
+// Shared memory per CTA: the pool (B x 32 x 16 B), WARPS staging areas
+// (32 x 16 B) and the pool's in-use bitmap.
+__host__ __device__ __forceinline__ size_t smem_cta_bytes(int buckets,
+                                                          int warps) {
+  return (size_t)buckets * kBucket * 16 + (size_t)warps * 32 * 16 +
+         (size_t)((buckets + 31) / 32) * 4;
+}
+
+// Main pass: persistent warps pull traces (longest first) from a global
+// counter; the CTA's warps share one shared-memory bucket pool.
+template <int WARPS>
+__global__ void __launch_bounds__(WARPS * 32, 1)
+    replay_narrow_kernel(const pm_req_t* __restrict__ reqs,
+                         const int64_t* __restrict__ offs,
+                         const pm_cfg_t* __restrict__ cfgs,
+                         const int32_t* __restrict__ cfg_of,
+                         pm_result_t* __restrict__ results,
+                         int64_t* __restrict__ timeline, u32* recs,
+                         pmb::Ctl* ctl, const int32_t* __restrict__ list,
+                         int n_traces, int32_t* __restrict__ overflow_list,
+                         int buckets, const unsigned* __restrict__ group_end,
+                         int n_groups, const volatile unsigned* ready) {
+  extern __shared__ __align__(16) char smem[];
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  const size_t E = (size_t)buckets * kBucket;
+  NPool P;
+  P.ka = reinterpret_cast<u64*>(smem);
+  P.ln = P.ka + E;
+  uint4* st = reinterpret_cast<uint4*>(smem + E * 16) + wib * 32;
+  unsigned* used =
+      reinterpret_cast<unsigned*>(smem + E * 16 + (size_t)WARPS * 32 * 16);
+  const int words = (buckets + 31) / 32;
+  for (int i = threadIdx.x; i < words; i += blockDim.x) used[i] = 0u;
+  __syncthreads();
+  NDir dir;
+  dir.cta_used = used;
+  dir.cta_words = words;
+  dir.cta_buckets = buckets;
+  for (;;) {
+    unsigned t = 0;
+    if (lane == 0) t = atomicAdd(&ctl->work[0], 1u);
+    t = __shfl_sync(kFull, t, 0);
+    if (t >= (unsigned)n_traces) break;
+    if (ready != nullptr) {
+      if (lane == 0) {
+        int g = 0;
+        while (g + 1 < n_groups && t >= group_end[g]) ++g;
+        while (ready[g] == 0u) __nanosleep(2000);
+      }
+      __syncwarp();
+    }
+    const int tr = list ? list[t] : (int)t;
+    replay_trace(tr, reqs, offs, cfgs, cfg_of, results, timeline, recs, P, dir,
+                 st, lane);
+    __syncwarp();
+    if (lane == 0 && results[tr].status == PM_POOL_OVERFLOW) {
+      const unsigned k = atomicAdd(&ctl->n_list[1], 1u);
+      overflow_list[k] = tr;
+    }
+  }
+}
+
+}  // namespace pmn
