@@ -31,7 +31,7 @@ int cuda_fail(cudaError_t e, const char* where) {
 }
 
 constexpr int kWarps = 12;        // wide main kernel (PM_REPLAY_WIDE=1)
-constexpr int kNarrowWarps = 16;  // narrow main kernel
+constexpr int kNarrowWarps = 20;  // narrow main kernel (PM_REPLAY_WARPS: 12, 16, 20, 24)
 constexpr size_t kBucket_host = 32;  // warps (traces in flight) per CTA, 1 CTA / SM
 constexpr int kRetryWarps = 1;
 constexpr int kMaxRetryWarps = 64;
@@ -97,7 +97,8 @@ int setup_kernel(int optin, int cap, int* buckets, size_t* smem, int* per_sm) {
 
 template <int W>
 int setup_narrow(int optin, int cap, int* buckets, size_t* smem, int* per_sm) {
-  int b = (int)(((size_t)optin - (size_t)W * 32 * 16 - 256) / (kBucket_host * 16));
+  int b = (int)(((size_t)optin - (size_t)W * pmn::kWarpStageBytes - 256) /
+                (kBucket_host * 16));
   if (cap > 0 && cap < b) b = cap;
   if (b < 2 * W) b = 2 * W;
   *buckets = b;
@@ -144,6 +145,8 @@ int query_occupancy(Occupancy* out) {
         rc = setup_narrow<12>(optin, cap, &o.buckets, &o.smem, &o.per_sm);
       else if (o.warps == 20)
         rc = setup_narrow<20>(optin, cap, &o.buckets, &o.smem, &o.per_sm);
+      else if (o.warps == 24)
+        rc = setup_narrow<24>(optin, cap, &o.buckets, &o.smem, &o.per_sm);
       else {
         o.warps = 16;
         rc = setup_narrow<16>(optin, cap, &o.buckets, &o.smem, &o.per_sm);
@@ -282,6 +285,8 @@ int replay_batch_impl(const pm_req_t* reqs, const int64_t* trace_offsets,
       PM_LAUNCH_NARROW(12);
     else if (occ.warps == 20)
       PM_LAUNCH_NARROW(20);
+    else if (occ.warps == 24)
+      PM_LAUNCH_NARROW(24);
     else
       PM_LAUNCH_NARROW(16);
   } else if (occ.warps == 12)

@@ -148,7 +148,7 @@ struct NDir {
     int p = -1;
     if (lane == 0) {
       for (int w = 0; w < cta_words && p < 0; ++w) {
-        unsigned v = cta_used[w];
+        unsigned v = *(volatile unsigned*)&cta_used[w];
         while (v != 0xffffffffu) {
           const int b = __ffs(~v) - 1;
           const unsigned old = atomicOr(&cta_used[w], 1u << b);
@@ -162,6 +162,28 @@ struct NDir {
       if (p >= cta_buckets) p = -1;
     }
     return __shfl_sync(kFull, p, 0);
+  }
+  // The CTA's pool is exhausted: wait for another warp to hand a bucket
+  // back (buckets empty out continuously as free blocks are taken), unless
+  // every warp replaying a trace in this CTA is itself waiting -- then -1
+  // (the trace escalates to the wide tiers).  ctr[0] waiting warps, ctr[1]
+  // active warps, after the bitmap.
+  __device__ __forceinline__ int alloc_phys_wait() {
+    int p = alloc_phys();
+    if (p >= 0) return p;
+    int* ctr = reinterpret_cast<int*>(cta_used + cta_words);
+    if (lane == 0) atomicAdd(&ctr[0], 1);
+    for (;;) {
+      __nanosleep(500);
+      p = alloc_phys();
+      if (p >= 0) break;
+      int stuck = 0;
+      if (lane == 0)
+        stuck = *(volatile int*)&ctr[0] >= *(volatile int*)&ctr[1];
+      if (__shfl_sync(kFull, stuck, 0)) break;
+    }
+    if (lane == 0) atomicSub(&ctr[0], 1);
+    return p;
   }
   __device__ __forceinline__ void free_phys(int p) {
     if (lane == 0) atomicAnd(&cta_used[p >> 5], ~(1u << (p & 31)));
@@ -268,8 +290,13 @@ __device__ __forceinline__ bool try_merge(const NPool& P, NDir& dir,
 __device__ __forceinline__ bool split_bucket(const NPool& P, NDir& dir, int d,
                                              const NRecs& rec, uint4* st,
                                              int hcmp, int lane) {
-  const int q = dir.full() ? -1 : dir.alloc_phys();
-  if (q < 0) return try_merge(P, dir, rec, st, hcmp, lane);
+  int q = dir.full() ? -1 : dir.alloc_phys();
+  if (q < 0) {
+    if (try_merge(P, dir, rec, st, hcmp, lane)) return true;
+    if (dir.full()) return false;
+    q = dir.alloc_phys_wait();
+    if (q < 0) return false;
+  }
   const int p = dir.phys(d);
   const int base = p * kBucket;
   const u64 ka = P.ka[base + lane];
@@ -306,7 +333,7 @@ __device__ __forceinline__ int pool_insert(const NPool& P, NDir& dir, NCtx& c,
                                            u64 ka, u64 links, const NRecs& rec,
                                            uint4* st, int hcmp, int lane) {
   if (dir.nb == 0) {
-    const int q = dir.alloc_phys();
+    const int q = dir.alloc_phys_wait();
     if (q < 0) return -1;
     dir.insert(0, 0ull, q, 0);
   }
@@ -369,9 +396,10 @@ __device__ __forceinline__ int pool_upsert(const NPool& P, NDir& dir, NCtx& c,
 }
 
 // Best fit (allocator.py:203-221): argmin ka over entries
-// with ru <= size_u and size_u - ru < span (span > 2^32: no bound).
+// with ru <= size_u and size_u - ru < span (span 0xFFFFFFFF: no bound --
+// size_u - ru <= kMaxU - 1 always).
 __device__ __forceinline__ int best_fit(const NPool& P, const NDir& dir,
-                                        u32 ru, u64 span, int lane) {
+                                        u32 ru, u32 span, int lane) {
   if (dir.nb == 0) return -1;
   const int d = dir.find((u64)ru << 32);
   {
@@ -379,7 +407,7 @@ __device__ __forceinline__ int best_fit(const NPool& P, const NDir& dir,
     const int id = p * kBucket + lane;
     const bool in = lane < dir.count(d);
     const u64 ka = in ? P.ka[id] : ~0ull;
-    const bool el = in && (u64)hi(ka) - (u64)ru < span;
+    const bool el = in && hi(ka) >= ru && hi(ka) - ru < span;
     const int w = argmin_pk(el, ka);
     if (w >= 0) return p * kBucket + w;
   }
@@ -393,7 +421,7 @@ __device__ __forceinline__ int best_fit(const NPool& P, const NDir& dir,
     const int w = argmin_pk(in, ka);
     if (w >= 0) {
       const u64 kw = __shfl_sync(kFull, ka, w);
-      if ((u64)hi(kw) - (u64)ru < span) return p * kBucket + w;
+      if (hi(kw) - ru < span) return p * kBucket + w;
     }
   }
   return -1;
@@ -426,12 +454,11 @@ __device__ __forceinline__ int find_release_candidate(const NPool& P,
 
 struct NCfg {
   const pm_cfg_t* cp;
-  u64 amask;         // alignment - 1 (bytes)
-  int s;             // unit shift
-  u64 span;          // best-fit window in units (> 2^32: unbounded)
-  u32 split_lim;     // splittable iff size_u <= split_lim
-  long long rel_thr; // stage-1 release threshold in units (max_split)
-  bool has_split;
+  u32 amask;     // alignment - 1 (bytes; alignment <= 2^31 in this pass)
+  u32 span;      // best-fit window in units (0xFFFFFFFF: unbounded)
+  u32 split_lim; // splittable iff size_u <= split_lim
+  u32 lim;       // largest rounded request in units (0: unit too large)
+  int s;         // unit shift
 };
 
 __device__ __forceinline__ void make_room(const NPool& P, NDir& dir, NCtx& c,
@@ -439,11 +466,14 @@ __device__ __forceinline__ void make_room(const NPool& P, NDir& dir, NCtx& c,
                                           const NRecs& rec, uint4* st,
                                           int hcmp, int lane) {
   const long long capacity = cf.cp->device_capacity;
-  int stage = cf.has_split ? 1 : 2;
+  const long long t = cf.cp->max_split_size;
+  // stage-1 threshold in units: size > t  <=>  size_u > floor(t / u)
+  const long long rel_thr = t >= 0 ? (long long)((u64)t >> cf.s) : -1;
+  int stage = t >= 0 ? 1 : 2;
   if (stage == 2 && c.reserved + seg <= capacity) return;
   for (;;) {
     if (stage == 1 && c.reserved + seg <= capacity) break;
-    const int id = find_release_candidate(P, dir, stage == 1 ? cf.rel_thr : -1,
+    const int id = find_release_candidate(P, dir, stage == 1 ? rel_thr : -1,
                                           lane);
     if (id < 0) {
       if (stage == 2 || c.reserved + seg <= capacity) break;
@@ -457,6 +487,56 @@ __device__ __forceinline__ void make_room(const NPool& P, NDir& dir, NCtx& c,
   }
 }
 
+// ---- request staging: 1-D TMA bulk copies into a per-warp double buffer ----
+
+__device__ __forceinline__ u32 smem_addr(const void* p) {
+  return (u32)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(u64* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+// one lane: arm the barrier with the byte count and start the copy
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, u32 bytes,
+                                          u64* bar) {
+  // order this warp's earlier generic reads of the buffer before the
+  // async-proxy write that refills it
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                   smem_addr(bar)),
+               "r"(bytes)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes "
+      "[%0], [%1], %2, [%3];" ::"r"(smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(u64* bar, u32 phase) {
+  u32 ok;
+  do {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;"
+        " selp.u32 %0, 1, 0, p; }"
+        : "=r"(ok)
+        : "r"(smem_addr(bar)), "r"(phase)
+        : "memory");
+  } while (!ok);
+}
+
+// Per-warp staging: two 32-request chunk buffers (TMA destinations), their
+// barriers, and the chunk's gathered records.
+struct NStage {
+  ulonglong2* buf;  // [2][32]
+  u64* bar;         // [2]
+  uint4* rec;       // [32]
+  u32 g;            // chunks consumed by this warp (buffer g & 1)
+};
+
 __device__ __forceinline__ int ctz64(long long v) {
   return __ffsll(v) - 1;
 }
@@ -467,13 +547,13 @@ __device__ __forceinline__ void replay_trace(
     int tr, const pm_req_t* __restrict__ reqs, const int64_t* __restrict__ offs,
     const pm_cfg_t* __restrict__ cfgs, const int32_t* __restrict__ cfg_of,
     pm_result_t* __restrict__ results, int64_t* __restrict__ timeline,
-    u32* rec_base, const NPool& P, NDir& dir, uint4* st, int lane) {
+    u32* rec_base, const NPool& P, NDir& dir, NStage& sg, int lane) {
   const long long e0 = offs[tr];
-  const long long n = offs[tr + 1] - e0;
+  const int n = (int)(offs[tr + 1] - e0);  // < 2^31 (pm_replay_batch)
   const pm_cfg_t* cp = cfgs + (cfg_of ? cfg_of[tr] : 0);
   NCfg cf;
   cf.cp = cp;
-  cf.amask = (u64)cp->alignment - 1;
+  cf.amask = (u32)(cp->alignment - 1);
   {
     int s = ctz64(cp->alignment);
     s = min(s, ctz64(cp->k_small_buffer));
@@ -482,22 +562,21 @@ __device__ __forceinline__ void replay_trace(
     cf.s = s;
   }
   const int s = cf.s;
-  const long long t = cp->max_split_size;
-  cf.has_split = t >= 0;
-  if (t >= 0) {
-    cf.span = ((u64)t + ((1ull << s) - 1)) >> s;  // ceil(t / u)
-    const u64 fl = (u64)t >> s;
-    cf.split_lim = fl > 0xFFFFFFFFull ? 0xFFFFFFFFu : (u32)fl;
-    cf.rel_thr = (long long)fl;
-  } else {
-    cf.span = 1ull << 33;
-    cf.split_lim = 0xFFFFFFFFu;
-    cf.rel_thr = -1;
+  // units above 16 MiB are left to the wide tiers altogether
+  cf.lim = s > 24 || cp->alignment > (1ll << 31) ? 0u : kMaxU;
+  {
+    const long long t = cp->max_split_size;
+    if (t >= 0) {
+      const u64 sp = ((u64)t + ((1ull << s) - 1)) >> s;  // ceil(t / u)
+      cf.span = sp > 0xFFFFFFFEull ? 0xFFFFFFFFu : (u32)sp;
+      const u64 fl = (u64)t >> s;
+      cf.split_lim = fl > 0xFFFFFFFFull ? 0xFFFFFFFFu : (u32)fl;
+    } else {
+      cf.span = 0xFFFFFFFFu;
+      cf.split_lim = 0xFFFFFFFFu;
+    }
   }
-  const u64 amask = cf.amask;
-  // largest request the encoding takes: rounded size_u <= kMaxU (units
-  // above 2^24 B are left to the wide tiers altogether)
-  const u64 size_cap = s > 24 ? 0ull : ((u64)kMaxU << s) - amask;
+  const u64 amask = cf.amask;  // widened at use
 
   NRecs rec;
   rec.base = rec_base + 4 * (size_t)e0;
@@ -513,40 +592,50 @@ __device__ __forceinline__ void replay_trace(
   c.next_base = 0;
   c.F = c.maxF = c.nseg = c.nseg_peak = 0;
   int status = PM_OK;
-  long long stop = -1;
+  int stop = -1;
 
-  const ulonglong2* rq = reinterpret_cast<const ulonglong2*>(reqs + e0);
-  ulonglong2 nxt = make_ulonglong2(0ull, 0xFFFFFFFFull);
-  if (lane < n) nxt = __ldg(rq + lane);
+  const pm_req_t* rq = reqs + e0;
+  const int nchunks = (n + 31) / 32;
+  if (lane == 0 && n > 0)
+    bulk_load(sg.buf + 32 * (sg.g & 1), rq, (u32)(n < 32 ? n : 32) * 16,
+              sg.bar + (sg.g & 1));
 
-  for (long long cbase = 0; cbase < n; cbase += 32) {
-    const ulonglong2 ev = nxt;
-    if (cbase + 32 + lane < n) nxt = __ldg(rq + cbase + 32 + lane);
-    const long long my_size = (long long)ev.x;
-    const int my_h = (int)lo(ev.y);
-    const unsigned my_ks = hi(ev.y);
-    const bool my_valid = cbase + lane < n;
-    const bool hok = my_valid && my_h >= 0 && (long long)my_h < n;
+  for (int k = 0; k < nchunks; ++k) {
+    const int cbase = 32 * k;
+    const u32 b = sg.g & 1;
+    mbar_wait(sg.bar + b, (sg.g >> 1) & 1);
+    if (lane == 0 && k + 1 < nchunks) {
+      // prefetch the next chunk into the other buffer (consumed last chunk)
+      const int rest = n - cbase - 32;
+      bulk_load(sg.buf + 32 * (b ^ 1), rq + cbase + 32,
+                (u32)(rest < 32 ? rest : 32) * 16, sg.bar + (b ^ 1));
+    }
+    const ulonglong2* cb = sg.buf + 32 * b;
+    const int cnt = min(n - cbase, 32);
+    const int my_h = lane < cnt ? (int)lo(cb[lane].y) : -1;
+    const bool hok = my_h >= 0 && my_h < n;
     uint4 r = make_uint4(0, 0, 0, 0);
     if (hok) r = *reinterpret_cast<const uint4*>(rec.word((u32)my_h, 0));
+    uint4* st = sg.rec;
     st[lane] = r;
     const int hcmp = hok ? my_h : -1;
     __syncwarp();
 
-    const int cnt = (int)((n - cbase) < 32 ? (n - cbase) : 32);
-    long long tl_r = 0, tl_a = 0;
-    int done = cnt;
+    ulonglong2 ev_next = cb[0];
     for (int j = 0; j < cnt; ++j) {
-      const long long size = __shfl_sync(kFull, my_size, j);
-      const int hj = __shfl_sync(kFull, my_h, j);
-      const unsigned ks = __shfl_sync(kFull, my_ks, j);
+      // the next request's load is issued before this one's dependent chain
+      const ulonglong2 ev = ev_next;
+      if (j + 1 < cnt) ev_next = cb[j + 1];
+      const long long size = (long long)ev.x;
+      const int hj = (int)lo(ev.y);
+      const unsigned ks = hi(ev.y);
       const unsigned kind = ks & 3u;
       const unsigned m = __ballot_sync(kFull, hcmp == hj) & ((1u << j) - 1u);
       const int src = m ? 31 - __clz(m) : j;
       int sts = PM_OK;
       if (kind >= PM_KIND_UNKNOWN) {
         sts = kind == PM_KIND_UNKNOWN ? PM_UNKNOWN_KIND : PM_MISSING_FIELD;
-      } else if ((unsigned)hj >= (unsigned long long)n) {
+      } else if ((unsigned)hj >= (unsigned)n) {
         sts = PM_BAD_HANDLE;
       } else {
         const uint4 rj = st[src];
@@ -565,7 +654,8 @@ __device__ __forceinline__ void replay_trace(
             sts = PM_DUPLICATE_HANDLE;
           } else if (size <= 0) {
             sts = PM_ZERO_SIZE;
-          } else if ((ks >> 2) != 0u || (u64)size > size_cap) {
+          } else if ((ks >> 2) != 0u ||
+                     ((((u64)size + amask) & ~amask) >> s) > (u64)cf.lim) {
             sts = PM_POOL_OVERFLOW;  // outside the encoding: wide tiers
           } else {
             const u32 ru = (u32)((((u64)size + amask) & ~amask) >> s);
@@ -707,21 +797,23 @@ __device__ __forceinline__ void replay_trace(
       if (sts != PM_OK) {
         status = sts;
         stop = cbase + j;
-        done = j;
         break;
       }
-      if (lane == j) {
-        tl_r = c.reserved;
-        tl_a = c.allocated;
-      }
+      if (timeline != nullptr && lane == j)
+        reinterpret_cast<longlong2*>(timeline)[e0 + (long long)(cbase + j)] =
+            make_longlong2(c.reserved, c.allocated);
       __syncwarp();
     }
-    if (timeline != nullptr && lane < done) {
-      const long long gi = e0 + cbase + lane;
-      reinterpret_cast<longlong2*>(timeline)[gi] = make_longlong2(tl_r, tl_a);
-    }
     __syncwarp();
-    if (status != PM_OK) break;
+    sg.g += 1;
+    if (status != PM_OK) {
+      if (k + 1 < nchunks) {
+        // drain the prefetch in flight so the buffer's phase stays in step
+        mbar_wait(sg.bar + (sg.g & 1), (sg.g >> 1) & 1);
+        sg.g += 1;
+      }
+      break;
+    }
   }
 
   dir.release_all();
@@ -742,12 +834,14 @@ __device__ __forceinline__ void replay_trace(
   }
 }
 
-// Shared memory per CTA: the pool (B x 32 x 16 B), WARPS staging areas
-// (32 x 16 B) and the pool's in-use bitmap.
+// Shared memory per CTA: the pool (B x 32 x 16 B), per warp a staging area
+// (two 512 B request buffers, 512 B of gathered records, two barriers),
+// and the pool's in-use bitmap.
+constexpr size_t kWarpStageBytes = 2 * 32 * 16 + 32 * 16 + 16;
 __host__ __device__ __forceinline__ size_t smem_cta_bytes(int buckets,
                                                           int warps) {
-  return (size_t)buckets * kBucket * 16 + (size_t)warps * 32 * 16 +
-         (size_t)((buckets + 31) / 32) * 4;
+  return (size_t)buckets * kBucket * 16 + (size_t)warps * kWarpStageBytes +
+         (size_t)((buckets + 31) / 32) * 4 + 8;
 }
 
 // Main pass: persistent warps pull traces (longest first) from a global
@@ -771,11 +865,22 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
   NPool P;
   P.ka = reinterpret_cast<u64*>(smem);
   P.ln = P.ka + E;
-  uint4* st = reinterpret_cast<uint4*>(smem + E * 16) + wib * 32;
-  unsigned* used =
-      reinterpret_cast<unsigned*>(smem + E * 16 + (size_t)WARPS * 32 * 16);
+  char* wst = smem + E * 16 + (size_t)wib * kWarpStageBytes;
+  NStage sg;
+  sg.buf = reinterpret_cast<ulonglong2*>(wst);
+  sg.rec = reinterpret_cast<uint4*>(wst + 2 * 32 * 16);
+  sg.bar = reinterpret_cast<u64*>(wst + 3 * 32 * 16);
+  sg.g = 0;
+  unsigned* used = reinterpret_cast<unsigned*>(smem + E * 16 +
+                                               (size_t)WARPS * kWarpStageBytes);
   const int words = (buckets + 31) / 32;
-  for (int i = threadIdx.x; i < words; i += blockDim.x) used[i] = 0u;
+  for (int i = threadIdx.x; i < words + 2; i += blockDim.x) used[i] = 0u;
+  int* active = reinterpret_cast<int*>(used + words) + 1;
+  if (lane == 0) {
+    mbar_init(sg.bar);
+    mbar_init(sg.bar + 1);
+    mbar_fence_init();
+  }
   __syncthreads();
   NDir dir;
   dir.cta_used = used;
@@ -795,9 +900,11 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
       __syncwarp();
     }
     const int tr = list ? list[t] : (int)t;
+    if (lane == 0) atomicAdd(active, 1);
     replay_trace(tr, reqs, offs, cfgs, cfg_of, results, timeline, recs, P, dir,
-                 st, lane);
+                 sg, lane);
     __syncwarp();
+    if (lane == 0) atomicSub(active, 1);
     if (lane == 0 && results[tr].status == PM_POOL_OVERFLOW) {
       const unsigned k = atomicAdd(&ctl->n_list[1], 1u);
       overflow_list[k] = tr;
