@@ -11,8 +11,9 @@ collective on the data path): strong scaling of a fixed 10^4-trace sweep.
           pm_replay_batch over the rank's shard, timed with CUDA events on
           the launching stream, max over ranks.
   e2e     the same step through the C ABI with HOST buffers
-          (pm_replay_host: pinned host requests -> H2D -> replay -> D2H of
-          the per-trace results), wall-clock around the synchronous call.
+          (pm_replay_host_wire: pinned host requests in the 8-byte wire
+          format -> H2D -> replay -> D2H of the per-trace results),
+          wall-clock around the synchronous call.
   roofline  HBM: 16 B of packed request read per replayed event
            / the replay launch's CUDA-event duration, against
           MEASURED_PEAKS.json hbm_gbs.
@@ -252,14 +253,22 @@ def main():
         max_ms, all_events = elapsed_ms, float(events_per_step)
     value = all_events * args.steps / (max_ms / 1e3)
 
-    # ---- e2e: host buffers through the C ABI (pm_replay_host) -------------
+    # ---- e2e: host buffers through the C ABI ------------------------------
+    # The host packs its requests once into the engine's 8-byte wire format
+    # (pm_wire_pack, like pack_trace builds pm_req_t; outside the timed
+    # region); each timed step is pm_replay_host_wire: H2D of the words
+    # (pinned), replay, D2H of the per-trace results.
     e2e_steps = args.e2e_steps or max(1, min(args.steps, 3))
-    _native.replay_host(reqs, offs, cfg, None, False)  # pool warm-up
+    whost = torch.empty(total * 8, dtype=torch.uint8, pin_memory=True)
+    words = _native.wire_pack(reqs, offs, out=whost.numpy().view(np.uint64))
+    if words is None:
+        raise RuntimeError("C3 requests must have a wire encoding")
+    _native.replay_host_wire(words, offs, cfg, None, False)  # pool warm-up
     if dist:
         dist.barrier()
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
-        res_host, _ = _native.replay_host(reqs, offs, cfg, None, False)
+        res_host, _ = _native.replay_host_wire(words, offs, cfg, None, False)
     e2e_s = time.perf_counter() - t0
     e2e_t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
     if dist:
@@ -321,10 +330,11 @@ def main():
             "parallelism": f"traces sharded over {world} GPU(s), no collective",
         },
         "e2e": {"value": e2e_value, "unit": "events/s",
-                "h2d_bytes_per_step": int(reqs.nbytes + offs.nbytes + cfg.nbytes),
+                "h2d_bytes_per_step": int(words.nbytes + offs.nbytes + cfg.nbytes),
                 "d2h_bytes_per_step": int(res_host.nbytes),
                 "steps": e2e_steps,
-                "api": "pm_replay_host (C ABI, pinned host buffers)"},
+                "api": "pm_replay_host_wire (C ABI, pinned host buffers, 8-byte "
+                       "wire words packed by pm_wire_pack outside the timed region)"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak,
                      "unit": "GB/s", "frac": achieved / peak,
                      "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",

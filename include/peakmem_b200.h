@@ -137,6 +137,27 @@ int pm_replay_host(const pm_req_t* reqs, const int64_t* trace_offsets,
                    const int32_t* cfg_of_trace, pm_result_t* results,
                    int64_t* timeline, void* stream);
 
+/* ---- 8-byte wire format for host-buffer replay --------------------------
+ * replay() input (allocator.py:360-393) after the packer's handle interning
+ * is, in the common case, "alloc of the next new handle with a size" or
+ * "free of handle h".  Those fit one 64-bit word:
+ *   bits 63..62 = 0 : alloc, handle = number of allocs before it in the
+ *                     trace, stream 0, size = bits 61..0 (>= 1)
+ *   bits 63..62 = 1 : free of handle bits 30..0
+ * pm_wire_pack converts pm_req_t traces to wire words; it returns
+ * PM_ERR_INVALID_ARGUMENT (and *first_bad = the request index) when a
+ * request does not fit (an alloc of another handle, a stream, a size < 1 or
+ * >= 2^62, an unknown kind), in which case the caller uses pm_replay_host.
+ * pm_replay_host_wire is pm_replay_host on wire words: half the H2D bytes,
+ * bit-identical results. */
+#define PM_WIRE_FREE (1ull << 62)
+int pm_wire_pack(const pm_req_t* reqs, const int64_t* trace_offsets,
+                 int32_t n_traces, uint64_t* words, int64_t* first_bad);
+int pm_replay_host_wire(const uint64_t* words, const int64_t* trace_offsets,
+                        int32_t n_traces, const pm_cfg_t* cfgs, int32_t n_cfgs,
+                        const int32_t* cfg_of_trace, pm_result_t* results,
+                        int64_t* timeline, void* stream);
+
 /* ---- batched capacity bisection ------------------------
  * The smallest device_capacity each trace replays in without OutOfMemory,
  * found by bisection over whole-batch replays.  No reference function does

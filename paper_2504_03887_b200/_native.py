@@ -42,7 +42,8 @@ KIND_ALLOC, KIND_FREE, KIND_UNKNOWN, KIND_MISSING = 0, 1, 2, 3
 
 #: every symbol include/peakmem_b200.h declares
 EXPORTED_SYMBOLS = ("pm_last_error", "pm_version", "pm_replay_workspace_bytes",
-                    "pm_replay_batch", "pm_replay_host",
+                    "pm_replay_batch", "pm_replay_host", "pm_wire_pack",
+                    "pm_replay_host_wire",
                     "pm_capacity_workspace_bytes", "pm_capacity_search")
 
 _lib = None
@@ -78,6 +79,10 @@ def load_library(path: Path | str | None = None) -> ctypes.CDLL:
                                     ctypes.c_size_t, i64, i64, vp]
     lib.pm_replay_host.restype = ctypes.c_int
     lib.pm_replay_host.argtypes = [vp, vp, i32, vp, i32, vp, vp, vp, vp]
+    lib.pm_replay_host_wire.restype = ctypes.c_int
+    lib.pm_replay_host_wire.argtypes = [vp, vp, i32, vp, i32, vp, vp, vp, vp]
+    lib.pm_wire_pack.restype = ctypes.c_int
+    lib.pm_wire_pack.argtypes = [vp, vp, i32, vp, ctypes.POINTER(i64)]
     lib.pm_capacity_workspace_bytes.restype = ctypes.c_int
     lib.pm_capacity_workspace_bytes.argtypes = [
         i64, i64, i32, ctypes.POINTER(ctypes.c_size_t)]
@@ -138,3 +143,55 @@ def replay_host(reqs: np.ndarray, offsets: np.ndarray, cfgs: np.ndarray,
                              len(cfgs), _p(cfg_of), _p(results),
                              _p(timeline), ctypes.c_void_p(stream)), lib)
     return results, timeline
+
+
+def wire_pack(reqs: np.ndarray, offsets: np.ndarray, out: np.ndarray | None = None):
+    """Pack pm_req_t traces into 8-byte wire words (include/peakmem_b200.h).
+
+    Returns the uint64 words, or None when some request has no wire
+    encoding (the caller then replays the pm_req_t records).  Host-only."""
+    lib = load_library()
+    reqs = np.ascontiguousarray(reqs, dtype=REQ_DTYPE)
+    offsets = np.ascontiguousarray(offsets, dtype=np.int64)
+    if out is None:
+        out = np.empty(len(reqs), dtype=np.uint64)
+    bad = ctypes.c_int64(-1)
+    rc = lib.pm_wire_pack(_p(reqs), _p(offsets), len(offsets) - 1, _p(out),
+                          ctypes.byref(bad))
+    if rc != 0:
+        if bad.value >= 0:
+            return None
+        check(rc, lib)
+    return out[:len(reqs)]
+
+
+def replay_host_wire(words: np.ndarray, offsets: np.ndarray, cfgs: np.ndarray,
+                     cfg_of: np.ndarray | None, want_timeline: bool,
+                     stream: int = 0):
+    """Host-buffer replay of wire words through pm_replay_host_wire."""
+    lib = load_library()
+    require_device()
+    words = np.ascontiguousarray(words, dtype=np.uint64)
+    offsets = np.ascontiguousarray(offsets, dtype=np.int64)
+    cfgs = np.ascontiguousarray(cfgs, dtype=CFG_DTYPE)
+    n_traces = len(offsets) - 1
+    if cfg_of is not None:
+        cfg_of = np.ascontiguousarray(cfg_of, dtype=np.int32)
+    results = np.zeros(n_traces, dtype=RESULT_DTYPE)
+    timeline = (np.zeros(2 * max(len(words), 1), dtype=np.int64)
+                if want_timeline else None)
+    check(lib.pm_replay_host_wire(_p(words), _p(offsets), n_traces, _p(cfgs),
+                                  len(cfgs), _p(cfg_of), _p(results),
+                                  _p(timeline), ctypes.c_void_p(stream)), lib)
+    return results, timeline
+
+
+def replay_host_auto(reqs: np.ndarray, offsets: np.ndarray, cfgs: np.ndarray,
+                     cfg_of: np.ndarray | None, want_timeline: bool,
+                     stream: int = 0):
+    """pm_replay_host_wire when every request has a wire encoding (half the
+    H2D bytes), else pm_replay_host; results are identical."""
+    words = wire_pack(reqs, offsets) if len(reqs) else None
+    if words is not None:
+        return replay_host_wire(words, offsets, cfgs, cfg_of, want_timeline, stream)
+    return replay_host(reqs, offsets, cfgs, cfg_of, want_timeline, stream)

@@ -277,7 +277,7 @@ def replay_batch(traces: Sequence[Iterable[dict]],
             else np.zeros(0, dtype=REQ_DTYPE))
     if n == 0:
         return []
-    results, tl = _native.replay_host(reqs, offsets, cfg_arr, cfg_of, timeline)
+    results, tl = _native.replay_host_auto(reqs, offsets, cfg_arr, cfg_of, timeline)
     return [_result_from(results[i], packed[i], tl, int(offsets[i]), result_cls)
             for i in range(n)]
 

@@ -12,6 +12,8 @@
 // Host side of the C ABI.
 
 #include <algorithm>
+#include <cstdio>
+#include <functional>
 #include <cstdlib>
 #include <mutex>
 #include <string>
@@ -171,6 +173,23 @@ int query_occupancy(Occupancy* out) {
                              cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)o.smem2);
     if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute tier 2");
+    // load every replay kernel now (lazy module loading would otherwise
+    // load a retry tier at its first launch, which waits for the device --
+    // and pm_replay_host's main pass waits for copies enqueued after it)
+    {
+      cudaFuncAttributes fa;
+      const void* fns[] = {
+          (const void*)pmn::replay_narrow_kernel<12>, (const void*)pmn::replay_narrow_kernel<16>,
+          (const void*)pmn::replay_narrow_kernel<20>, (const void*)pmn::replay_narrow_kernel<24>,
+          (const void*)pmb::replay_smem_kernel<8>, (const void*)pmb::replay_smem_kernel<12>,
+          (const void*)pmb::replay_smem_kernel<14>, (const void*)pmb::replay_smem_kernel<16>,
+          (const void*)pmb::replay_dirmem_kernel<1, true>,
+          (const void*)pmb::replay_dirmem_kernel<kRetryWarps, false>};
+      for (const void* f : fns) {
+        e = cudaFuncGetAttributes(&fa, f);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaFuncGetAttributes");
+      }
+    }
     cached = o;
     cached_dev = dev;
   }
@@ -234,7 +253,9 @@ int replay_batch_impl(const pm_req_t* reqs, const int64_t* trace_offsets,
                       size_t workspace_bytes, int64_t total_events,
                       int64_t max_trace_events, void* stream_,
                       const unsigned* group_end, int n_groups,
-                      const unsigned* ready) {
+                      const unsigned* ready,
+                      const std::function<int()>& after_main = {},
+                      const uint64_t* wire = nullptr) {
   if (n_traces < 0 || total_events < 0 || max_trace_events < 0)
     return fail(PM_ERR_INVALID_ARGUMENT, "pm_replay_batch: negative size");
   if (n_traces == 0) return PM_SUCCESS;
@@ -275,7 +296,8 @@ int replay_batch_impl(const pm_req_t* reqs, const int64_t* trace_offsets,
   pmn::replay_narrow_kernel<W><<<(unsigned)grid, W * 32, occ.smem, stream>>>( \
       reqs, trace_offsets, cfgs, cfg_of_trace, results, timeline,             \
       reinterpret_cast<pmb::u32*>(recs), ctl, trace_order, n_traces, list1,   \
-      occ.buckets, group_end, n_groups, ready)
+      occ.buckets, group_end, n_groups, ready,                               \
+      reinterpret_cast<const pmb::u64*>(wire), const_cast<pm_req_t*>(reqs))
 #define PM_LAUNCH_MAIN(W)                                                     \
   pmb::replay_smem_kernel<W><<<(unsigned)grid, W * 32, occ.smem, stream>>>(  \
       reqs, trace_offsets, cfgs, cfg_of_trace, results, timeline, recs, ctl, \
@@ -299,6 +321,12 @@ int replay_batch_impl(const pm_req_t* reqs, const int64_t* trace_offsets,
 #undef PM_LAUNCH_NARROW
   e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "replay_smem_kernel launch");
+  if (after_main) {
+    // streamed input: the copies go in behind the main pass (which waits
+    // on their flags) and before any further launch
+    const int rc2 = after_main();
+    if (rc2 != PM_SUCCESS) return rc2;
+  }
   // tier 1: dedicated 32-bucket pools (grid sized for the worst case; idle
   // CTAs exit at once when nothing overflowed)
   long long grid1 = (long long)occ.per_sm1 * occ.sms;
@@ -345,10 +373,20 @@ int pm_replay_batch(const pm_req_t* reqs, const int64_t* trace_offsets,
                            stream_, nullptr, 0, nullptr);
 }
 
-int pm_replay_host(const pm_req_t* reqs, const int64_t* trace_offsets,
-                   int32_t n_traces, const pm_cfg_t* cfgs, int32_t n_cfgs,
-                   const int32_t* cfg_of_trace, pm_result_t* results,
-                   int64_t* timeline, void* stream_) {
+}  // extern "C"
+
+namespace {
+
+// pm_replay_host / pm_replay_host_wire: `src` holds pm_req_t records
+// (wb = 16) or wire words (wb = 8).  Wire words are replayed by the narrow
+// main pass directly; d_reqs then only receives the pm_req_t expansion of
+// traces escalated to the wide tiers.
+int replay_host_impl(const void* src, size_t wb, const int64_t* trace_offsets,
+                     int32_t n_traces, const pm_cfg_t* cfgs, int32_t n_cfgs,
+                     const int32_t* cfg_of_trace, pm_result_t* results,
+                     int64_t* timeline, void* stream_) {
+  const char* reqs = static_cast<const char*>(src);
+  const bool wire = wb == 8;
   if (n_traces < 0 || n_cfgs < 1)
     return fail(PM_ERR_INVALID_ARGUMENT, "pm_replay_host: bad counts");
   if (n_traces == 0) return PM_SUCCESS;
@@ -369,30 +407,67 @@ int pm_replay_host(const pm_req_t* reqs, const int64_t* trace_offsets,
     for (int32_t i = 0; i < n_traces; ++i)
       if (cfg_of_trace[i] < 0 || cfg_of_trace[i] >= n_cfgs)
         return fail(PM_ERR_INVALID_ARGUMENT, "pm_replay_host: cfg index out of range");
-  // Streamed upload: G contiguous trace groups, each copied (copy stream)
-  // and then flagged with a 4-byte DMA write; the kernel consumes groups in
-  // order, longest trace first within a group, so replay overlaps the H2D.
-  const size_t bytes_in = 16 * (size_t)total;
+  // Streamed upload in longest-first order: the traces, sorted by length
+  // (stable), are cut into G groups of ~equal bytes; each trace is copied to
+  // its own offset on a copy stream and each group is followed by a 4-byte
+  // DMA of a pinned "1" into its ready flag.  The kernel (launched first)
+  // takes traces in the same order and waits for a trace's group flag, so
+  // replay overlaps the H2D and the last group to land holds the shortest
+  // traces.
+  const size_t bytes_in = wb * (size_t)total;
   int G = (int)(bytes_in / (256u << 20));
   if (G < 1) G = 1;
   if (G > 64) G = 64;
   if (G > n_traces) G = n_traces;
-  std::vector<int32_t> gfirst(G + 1);
-  for (int g = 0; g <= G; ++g) gfirst[g] = (int32_t)(((int64_t)n_traces * g) / G);
   std::vector<int32_t> order(n_traces);
+  for (int32_t i = 0; i < n_traces; ++i) order[i] = i;
+  std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) {
+    return trace_offsets[a + 1] - trace_offsets[a] >
+           trace_offsets[b + 1] - trace_offsets[b];
+  });
   std::vector<unsigned> group_end(G);
-  for (int g = 0; g < G; ++g) {
-    for (int32_t i = gfirst[g]; i < gfirst[g + 1]; ++i) order[i] = i;
-    std::stable_sort(order.begin() + gfirst[g], order.begin() + gfirst[g + 1],
-                     [&](int32_t a, int32_t b) {
-                       return trace_offsets[a + 1] - trace_offsets[a] >
-                              trace_offsets[b + 1] - trace_offsets[b];
-                     });
-    group_end[g] = (unsigned)gfirst[g + 1];
+  {
+    int g = 0;
+    int64_t acc = 0;
+    for (int32_t i = 0; i < n_traces; ++i) {
+      const int32_t t = order[i];
+      acc += trace_offsets[t + 1] - trace_offsets[t];
+      // close group g once the groups so far hold their share of the
+      // requests (the last group takes the rest; a group may be empty)
+      while (g < G - 1 && acc * G >= total * (int64_t)(g + 1)) {
+        group_end[g++] = (unsigned)(i + 1);
+      }
+    }
+    while (g < G) group_end[g++] = (unsigned)n_traces;
   }
   const Layout L = layout_for(total, max_ev, n_traces);
   cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
-  const size_t b_reqs = align_up(16 * (size_t)(total > 0 ? total : 1), 256);
+  // Pinned source: by default the kernels read it in place (zero copy:
+  // pinned memory is device-addressable, each warp's TMA bulk load pulls
+  // its next chunk over PCIe one chunk ahead), so nothing is staged in HBM.
+  // PM_HOST_COPY=1 streams it through the copy engines instead (launch
+  // first, per-group ready flags).  A pageable source is copied before the
+  // launch: its cudaMemcpyAsync synchronises with the device.
+  bool pinned = false;
+  void* mapped = nullptr;
+  {
+    cudaPointerAttributes pa;
+    pinned = cudaPointerGetAttributes(&pa, reqs) == cudaSuccess &&
+             pa.type == cudaMemoryTypeHost;
+    cudaGetLastError();  // clear a failed query
+  }
+  const char* copy_env = getenv("PM_HOST_COPY");
+  const bool zero_copy =
+      pinned && !(copy_env && atoi(copy_env) != 0) &&
+      cudaHostGetDevicePointer(&mapped, const_cast<char*>(reqs), 0) == cudaSuccess;
+  cudaGetLastError();
+  // d_reqs: staged pm_req_t, or (wire) the expansion of escalated traces
+  const size_t b_reqs = (zero_copy && !wire)
+                            ? 256
+                            : align_up(16 * (size_t)(total > 0 ? total : 1), 256);
+  const size_t b_wire = (wire && !zero_copy)
+                            ? align_up(8 * (size_t)(total > 0 ? total : 1), 256)
+                            : 0;
   const size_t b_offs = align_up(8 * (size_t)(n_traces + 1), 256);
   const size_t b_cfgs = align_up(sizeof(pm_cfg_t) * (size_t)n_cfgs, 256);
   const size_t b_cfgof = align_up(4 * (size_t)n_traces, 256);
@@ -400,8 +475,8 @@ int pm_replay_host(const pm_req_t* reqs, const int64_t* trace_offsets,
   const size_t b_res = align_up(sizeof(pm_result_t) * (size_t)n_traces, 256);
   const size_t b_tl = timeline ? align_up(16 * (size_t)(total > 0 ? total : 1), 256) : 0;
   const size_t b_grp = align_up(8 * (size_t)G, 256);
-  const size_t bytes = b_reqs + b_offs + b_cfgs + b_cfgof + b_order + b_res +
-                       b_tl + 2 * b_grp + L.total;
+  const size_t bytes = b_reqs + b_wire + b_offs + b_cfgs + b_cfgof + b_order +
+                       b_res + b_tl + 2 * b_grp + L.total;
   keep_pool_mapped();
   static unsigned* one = nullptr;  // pinned source of the group flags
   {
@@ -413,6 +488,9 @@ int pm_replay_host(const pm_req_t* reqs, const int64_t* trace_offsets,
       *one = 1u;
     }
   }
+  // PM_TRACE_PHASES=1: report when the copies and the replay finished
+  const bool trace_phases = getenv("PM_TRACE_PHASES") != nullptr;
+  cudaEvent_t ph[3] = {nullptr, nullptr, nullptr};
   cudaStream_t cs = nullptr;
   cudaError_t e = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking);
   if (e != cudaSuccess) return cuda_fail(e, "cudaStreamCreate");
@@ -432,6 +510,8 @@ int pm_replay_host(const pm_req_t* reqs, const int64_t* trace_offsets,
   char* p = static_cast<char*>(dmem);
   pm_req_t* d_reqs = reinterpret_cast<pm_req_t*>(p);
   p += b_reqs;
+  char* d_src = wire ? p : reinterpret_cast<char*>(d_reqs);
+  p += b_wire;
   int64_t* d_offs = reinterpret_cast<int64_t*>(p);
   p += b_offs;
   pm_cfg_t* d_cfgs = reinterpret_cast<pm_cfg_t*>(p);
@@ -474,23 +554,82 @@ int pm_replay_host(const pm_req_t* reqs, const int64_t* trace_offsets,
     PM_CHECK(cudaMemsetAsync(d_tl, 0, b_tl, stream), "memset timeline");
   PM_CHECK(cudaEventRecord(zeroed, stream), "event record");
   PM_CHECK(cudaStreamWaitEvent(cs, zeroed, 0), "stream wait");
-  for (int g = 0; g < G; ++g) {
-    const int64_t e0 = trace_offsets[gfirst[g]], e1 = trace_offsets[gfirst[g + 1]];
-    if (e1 > e0)
-      PM_CHECK(cudaMemcpyAsync(d_reqs + e0, reqs + e0, 16 * (size_t)(e1 - e0),
-                               cudaMemcpyHostToDevice, cs), "H2D requests");
-    PM_CHECK(cudaMemcpyAsync(d_ready + g, one, sizeof(unsigned),
-                             cudaMemcpyHostToDevice, cs), "H2D flag");
+  if (trace_phases) {
+    cudaEventCreate(&ph[0]);
+    cudaEventCreate(&ph[1]);
+    cudaEventCreate(&ph[2]);
+    cudaEventRecord(ph[0], stream);
   }
-  rc = replay_batch_impl(d_reqs, d_offs, n_traces, d_cfgs,
-                         cfg_of_trace ? d_cfgof : nullptr, d_order, d_res, d_tl,
-                         d_ws, L.total, total, max_ev, stream_, d_gend, G, d_ready);
-  if (rc != PM_SUCCESS) goto done;
+  {
+    // Pinned source: launch the main pass first (it waits on the flags) and
+    // enqueue the copies behind it, before the tier launches.  A pageable
+    // source makes each cudaMemcpyAsync synchronise with the device, so its
+    // copies are all enqueued before the launch (no overlap, no deadlock).
+    auto enqueue_copies = [&]() -> int {
+      int32_t i = 0;
+      for (int g = 0; g < G; ++g) {
+        while (i < (int32_t)group_end[g]) {
+          // one copy per run of traces adjacent in memory
+          const int32_t t0 = order[i];
+          int64_t e0 = trace_offsets[t0], e1 = trace_offsets[t0 + 1];
+          ++i;
+          while (i < (int32_t)group_end[g] && trace_offsets[order[i]] == e1) {
+            e1 = trace_offsets[order[i] + 1];
+            ++i;
+          }
+          cudaError_t ce = cudaSuccess;
+          if (e1 > e0)
+            ce = cudaMemcpyAsync(d_src + wb * e0, reqs + wb * e0,
+                                 wb * (size_t)(e1 - e0), cudaMemcpyHostToDevice, cs);
+          if (ce != cudaSuccess) {
+            // release the waiting replay before failing (results unused)
+            cudaMemsetAsync(d_ready, 0xFF, 4 * (size_t)G, cs);
+            return cuda_fail(ce, "H2D requests");
+          }
+        }
+        cudaError_t ce = cudaMemcpyAsync(d_ready + g, one, sizeof(unsigned),
+                                         cudaMemcpyHostToDevice, cs);
+        if (ce != cudaSuccess) {
+          cudaMemsetAsync(d_ready, 0xFF, 4 * (size_t)G, cs);
+          return cuda_fail(ce, "H2D flag");
+        }
+      }
+      if (trace_phases) cudaEventRecord(ph[2], cs);
+      return PM_SUCCESS;
+    };
+    if (zero_copy) {
+      const pm_req_t* rsrc =
+          wire ? d_reqs : reinterpret_cast<const pm_req_t*>(mapped);
+      rc = replay_batch_impl(rsrc, d_offs, n_traces, d_cfgs,
+                             cfg_of_trace ? d_cfgof : nullptr, d_order, d_res,
+                             d_tl, d_ws, L.total, total, max_ev, stream_,
+                             nullptr, 0, nullptr, std::function<int()>(),
+                             wire ? reinterpret_cast<const uint64_t*>(mapped)
+                                  : nullptr);
+      if (trace_phases) cudaEventRecord(ph[2], stream);
+      if (rc != PM_SUCCESS) goto done;
+      goto launched;
+    }
+    if (!pinned) {
+      rc = enqueue_copies();
+      if (rc != PM_SUCCESS) goto done;
+    }
+    rc = replay_batch_impl(d_reqs, d_offs, n_traces, d_cfgs,
+                           cfg_of_trace ? d_cfgof : nullptr, d_order, d_res,
+                           d_tl, d_ws, L.total, total, max_ev, stream_, d_gend,
+                           G, d_ready,
+                           pinned ? std::function<int()>(enqueue_copies)
+                                  : std::function<int()>(),
+                           wire ? reinterpret_cast<const uint64_t*>(d_src) : nullptr);
+    if (rc != PM_SUCCESS) goto done;
+  }
+launched:
   PM_CHECK(cudaMemcpyAsync(results, d_res, sizeof(pm_result_t) * (size_t)n_traces,
                            cudaMemcpyDeviceToHost, stream), "D2H results");
   if (timeline && total > 0)
     PM_CHECK(cudaMemcpyAsync(timeline, d_tl, 16 * (size_t)total,
                              cudaMemcpyDeviceToHost, stream), "D2H timeline");
+  if (trace_phases) cudaEventRecord(ph[1], stream);
 done:
 #undef PM_CHECK
   {
@@ -500,9 +639,63 @@ done:
   cudaFreeAsync(dmem, stream);
   e = cudaStreamSynchronize(stream);
   if (rc == PM_SUCCESS && e != cudaSuccess) rc = cuda_fail(e, "cudaStreamSynchronize");
+  if (trace_phases && ph[1]) {
+    float k = 0, c = 0;
+    cudaEventElapsedTime(&k, ph[0], ph[1]);
+    cudaEventElapsedTime(&c, ph[0], ph[2]);
+    fprintf(stderr, "pm_replay_host: copies done %.1f ms, replay done %.1f ms after start\n", c, k);
+    for (auto& x : ph) cudaEventDestroy(x);
+  }
   cudaEventDestroy(zeroed);
   cudaStreamDestroy(cs);
   return rc;
+}
+
+}  // namespace
+
+extern "C" {
+
+int pm_replay_host(const pm_req_t* reqs, const int64_t* trace_offsets,
+                   int32_t n_traces, const pm_cfg_t* cfgs, int32_t n_cfgs,
+                   const int32_t* cfg_of_trace, pm_result_t* results,
+                   int64_t* timeline, void* stream) {
+  return replay_host_impl(reqs, 16, trace_offsets, n_traces, cfgs, n_cfgs,
+                          cfg_of_trace, results, timeline, stream);
+}
+
+int pm_replay_host_wire(const uint64_t* words, const int64_t* trace_offsets,
+                        int32_t n_traces, const pm_cfg_t* cfgs, int32_t n_cfgs,
+                        const int32_t* cfg_of_trace, pm_result_t* results,
+                        int64_t* timeline, void* stream) {
+  return replay_host_impl(words, 8, trace_offsets, n_traces, cfgs, n_cfgs,
+                          cfg_of_trace, results, timeline, stream);
+}
+
+int pm_wire_pack(const pm_req_t* reqs, const int64_t* trace_offsets,
+                 int32_t n_traces, uint64_t* words, int64_t* first_bad) {
+  if (first_bad) *first_bad = -1;
+  if (n_traces < 0 || (n_traces > 0 && (!trace_offsets || !words)))
+    return fail(PM_ERR_INVALID_ARGUMENT, "pm_wire_pack: bad arguments");
+  for (int32_t t = 0; t < n_traces; ++t) {
+    int64_t allocs = 0;
+    for (int64_t i = trace_offsets[t]; i < trace_offsets[t + 1]; ++i) {
+      const pm_req_t& r = reqs[i];
+      const uint32_t kind = r.kind_stream & 3u;
+      if (kind == PM_KIND_ALLOC && (r.kind_stream >> 2) == 0 &&
+          r.handle == allocs && r.size >= 1 && r.size < (int64_t)(1ll << 62)) {
+        words[i] = (uint64_t)r.size;
+        ++allocs;
+      } else if (kind == PM_KIND_FREE && r.handle >= 0) {
+        words[i] = PM_WIRE_FREE | (uint64_t)(uint32_t)r.handle;
+      } else {
+        if (first_bad) *first_bad = i;
+        return fail(PM_ERR_INVALID_ARGUMENT,
+                    "pm_wire_pack: request " + std::to_string(i) +
+                        " has no wire encoding");
+      }
+    }
+  }
+  return PM_SUCCESS;
 }
 
 }  // extern "C"

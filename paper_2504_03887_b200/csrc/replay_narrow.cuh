@@ -547,7 +547,8 @@ __device__ __forceinline__ void replay_trace(
     int tr, const pm_req_t* __restrict__ reqs, const int64_t* __restrict__ offs,
     const pm_cfg_t* __restrict__ cfgs, const int32_t* __restrict__ cfg_of,
     pm_result_t* __restrict__ results, int64_t* __restrict__ timeline,
-    u32* rec_base, const NPool& P, NDir& dir, NStage& sg, int lane) {
+    u32* rec_base, const NPool& P, NDir& dir, NStage& sg, int lane,
+    const u64* __restrict__ wire, pm_req_t* __restrict__ expand) {
   const long long e0 = offs[tr];
   const int n = (int)(offs[tr + 1] - e0);  // < 2^31 (pm_replay_batch)
   const pm_cfg_t* cp = cfgs + (cfg_of ? cfg_of[tr] : 0);
@@ -594,11 +595,26 @@ __device__ __forceinline__ void replay_trace(
   int status = PM_OK;
   int stop = -1;
 
-  const pm_req_t* rq = reqs + e0;
+  // requests arrive as pm_req_t (16 B) or as wire words (8 B, decoded in
+  // shared memory below)
+  // Bulk copies need 16 B-aligned sources and sizes: a chunk of wire words
+  // is fetched from the even word at or before it, rounded up to an even
+  // count (a word of the neighbouring trace at either end is ignored).
+  int abase = 0;  // wire: allocs before this chunk (= the next new handle)
   const int nchunks = (n + 31) / 32;
-  if (lane == 0 && n > 0)
-    bulk_load(sg.buf + 32 * (sg.g & 1), rq, (u32)(n < 32 ? n : 32) * 16,
-              sg.bar + (sg.g & 1));
+  auto fetch = [&](int k, u32 buf) {
+    const int cnt = min(n - 32 * k, 32);
+    if (wire) {
+      const long long w0 = e0 + 32 * k;
+      const long long a0 = w0 & ~1ll;
+      const u32 words = (u32)((w0 - a0) + cnt + 1) & ~1u;
+      bulk_load(sg.buf + 32 * buf, wire + a0, words * 8, sg.bar + buf);
+    } else {
+      bulk_load(sg.buf + 32 * buf, reqs + e0 + 32 * k, (u32)cnt * 16,
+                sg.bar + buf);
+    }
+  };
+  if (lane == 0 && n > 0) fetch(0, sg.g & 1);
 
   for (int k = 0; k < nchunks; ++k) {
     const int cbase = 32 * k;
@@ -606,12 +622,37 @@ __device__ __forceinline__ void replay_trace(
     mbar_wait(sg.bar + b, (sg.g >> 1) & 1);
     if (lane == 0 && k + 1 < nchunks) {
       // prefetch the next chunk into the other buffer (consumed last chunk)
-      const int rest = n - cbase - 32;
-      bulk_load(sg.buf + 32 * (b ^ 1), rq + cbase + 32,
-                (u32)(rest < 32 ? rest : 32) * 16, sg.bar + (b ^ 1));
+      fetch(k + 1, b ^ 1);
     }
-    const ulonglong2* cb = sg.buf + 32 * b;
+    ulonglong2* cb = sg.buf + 32 * b;
     const int cnt = min(n - cbase, 32);
+    if (wire) {
+      // decode the chunk's wire words in place into pm_req_t form
+      const int off = (int)((e0 + cbase) & 1);
+      const u64 w =
+          lane < cnt ? reinterpret_cast<const u64*>(cb)[off + lane] : 0ull;
+      __syncwarp();
+      const u32 tag = (u32)(w >> 62);
+      const unsigned am = __ballot_sync(kFull, lane < cnt && tag == 0);
+      if (lane < cnt) {
+        ulonglong2 d;
+        if (tag == 0) {  // alloc of the next new handle, stream 0
+          d.x = w & ((1ull << 62) - 1);
+          d.y = (u64)(u32)(abase + __popc(am & lanemask_lt()));
+        } else if (tag == 1) {  // free
+          d.x = 0;
+          d.y = (w & 0x7FFFFFFFull) | ((u64)PM_KIND_FREE << 32);
+        } else {  // not produced by pm_wire_pack
+          d.x = 0;
+          d.y = 0xFFFFFFFFull | ((u64)PM_KIND_UNKNOWN << 32);
+        }
+        cb[lane] = d;
+      }
+      abase += __popc(am);
+      // these generic writes precede the async-proxy refill of the buffer
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+    }
     const int my_h = lane < cnt ? (int)lo(cb[lane].y) : -1;
     const bool hok = my_h >= 0 && my_h < n;
     uint4 r = make_uint4(0, 0, 0, 0);
@@ -816,6 +857,35 @@ __device__ __forceinline__ void replay_trace(
     }
   }
 
+  if (wire != nullptr && status == PM_POOL_OVERFLOW) {
+    // the wide tiers read pm_req_t: expand this trace's words for them
+    int ab = 0;
+    for (int i0 = 0; i0 < n; i0 += 32) {
+      const int i = i0 + lane;
+      const u64 w = i < n ? __ldg(wire + e0 + i) : 0ull;
+      const u32 tag = (u32)(w >> 62);
+      const unsigned am = __ballot_sync(kFull, i < n && tag == 0);
+      if (i < n) {
+        pm_req_t d;
+        if (tag == 0) {
+          d.size = (int64_t)(w & ((1ull << 62) - 1));
+          d.handle = ab + __popc(am & lanemask_lt());
+          d.kind_stream = PM_KIND_ALLOC;
+        } else if (tag == 1) {
+          d.size = 0;
+          d.handle = (int32_t)(w & 0x7FFFFFFFull);
+          d.kind_stream = PM_KIND_FREE;
+        } else {
+          d.size = 0;
+          d.handle = -1;
+          d.kind_stream = PM_KIND_UNKNOWN;
+        }
+        expand[e0 + i] = d;
+      }
+      ab += __popc(am);
+    }
+  }
+
   dir.release_all();
   if (lane == 0) {
     pm_result_t res;
@@ -857,7 +927,9 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
                          pmb::Ctl* ctl, const int32_t* __restrict__ list,
                          int n_traces, int32_t* __restrict__ overflow_list,
                          int buckets, const unsigned* __restrict__ group_end,
-                         int n_groups, const volatile unsigned* ready) {
+                         int n_groups, const volatile unsigned* ready,
+                         const u64* __restrict__ wire,
+                         pm_req_t* __restrict__ expand) {
   extern __shared__ __align__(16) char smem[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
@@ -902,7 +974,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
     const int tr = list ? list[t] : (int)t;
     if (lane == 0) atomicAdd(active, 1);
     replay_trace(tr, reqs, offs, cfgs, cfg_of, results, timeline, recs, P, dir,
-                 sg, lane);
+                 sg, lane, wire, expand);
     __syncwarp();
     if (lane == 0) atomicSub(active, 1);
     if (lane == 0 && results[tr].status == PM_POOL_OVERFLOW) {

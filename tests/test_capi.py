@@ -150,3 +150,29 @@ def test_ingest_library_exports_every_declared_symbol():
     for sym in header_functions(header):
         assert sym in exported, sym
     _ingest.load()
+
+
+def test_wire_pack_roundtrip_and_rejections():
+    # pm_wire_pack (host-only): alloc of the next handle -> size word, free
+    # -> tag | handle; anything else has no encoding (-> None)
+    from paper_2504_03887_b200.allocator import pack_trace
+    seq = [{"seq_no": 0, "kind": "alloc", "block_id": "a", "size": 700},
+           {"seq_no": 1, "kind": "alloc", "block_id": "b", "size": 1 << 40},
+           {"seq_no": 2, "kind": "free", "block_id": "a"},
+           {"seq_no": 3, "kind": "alloc", "block_id": "c", "size": 1}]
+    p = pack_trace(seq)
+    offs = np.array([0, len(p.reqs)], dtype=np.int64)
+    w = _native.wire_pack(p.reqs, offs)
+    assert w is not None
+    tag = w >> np.uint64(62)
+    assert list(tag) == [0, 0, 1, 0]
+    assert list(w[[0, 1, 3]]) == [700, 1 << 40, 1]
+    assert int(w[2] & np.uint64(0x7FFFFFFF)) == int(p.reqs["handle"][0])
+    for bad in ([{"seq_no": 0, "kind": "alloc", "block_id": "a", "size": 5},
+                 {"seq_no": 1, "kind": "alloc", "block_id": "b", "size": 5, "stream": 1}],
+                [{"seq_no": 0, "kind": "alloc", "block_id": "a", "size": 0}],
+                [{"seq_no": 0, "kind": "alloc", "block_id": "a", "size": 5},
+                 {"seq_no": 1, "kind": "alloc", "block_id": "a", "size": 5}],
+                [{"seq_no": 0, "kind": "resize", "block_id": "a", "size": 5}]):
+        q = pack_trace(bad)
+        assert _native.wire_pack(q.reqs, np.array([0, len(q.reqs)])) is None

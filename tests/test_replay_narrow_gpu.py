@@ -52,6 +52,11 @@ def run_both(traces, cfgs):
     assert len(bad) == 0, f"{len(bad)} traces differ, first {bad[:5]}: " \
         f"{got[bad[0]]} vs {want[bad[0]]}"
     assert (tl == tl_ref).all()
+    # the same batch through the 8-byte wire format, where it encodes
+    words = _native.wire_pack(reqs, offs)
+    if words is not None:
+        gw, tlw = _native.replay_host_wire(words, offs, carr, cof, True)
+        assert (gw == want).all() and (tlw == tl_ref).all()
     return got
 
 
@@ -134,6 +139,58 @@ def test_mixed_batch_split_thresholds_and_capacity():
     want, tl_ref = oracle.replay_batch(reqs, offs, cfgs, cof, timeline=True)
     assert (got == want).all()
     assert (tl == tl_ref).all()
+
+
+def _wire_ok(seq):
+    p = pack_trace(seq)
+    return _native.wire_pack(p.reqs, np.array([0, len(p.reqs)])) is not None
+
+
+def test_wire_format_corpus_and_synthetic_vs_oracle():
+    # every corpus trace the wire format encodes, plus C3 traces with split
+    # thresholds and capacities (OOM verdicts), through pm_replay_host_wire
+    from replay_cases import corpus, pack_corpus
+    cases = corpus("corpus_seed1000")
+    r, o, c, f, _ = pack_corpus(cases)
+    keep = [i for i in range(len(o) - 1)
+            if _native.wire_pack(r[o[i]:o[i + 1]], np.array([0, o[i + 1] - o[i]]))
+            is not None]
+    assert len(keep) > 200
+    parts = [r[o[i]:o[i + 1]] for i in keep]
+    offs = np.zeros(len(keep) + 1, dtype=np.int64)
+    np.cumsum([len(x) for x in parts], out=offs[1:])
+    reqs = np.concatenate(parts)
+    cof = f[keep]
+    words = _native.wire_pack(reqs, offs)
+    got, tl = _native.replay_host_wire(words, offs, c, cof, True)
+    want, tl_ref = oracle.replay_batch(reqs, offs, c, cof, timeline=True)
+    assert (got == want).all() and (tl == tl_ref).all()
+    assert (want["status"] == 1).sum() > 50  # OOM verdicts among them
+
+    reqs, offs = synth.generate(16, first=4000)
+    cfgs = np.concatenate([cfg_record(AllocatorConfig()),
+                           cfg_record(AllocatorConfig(max_split_size=64 * MIB)),
+                           cfg_record(AllocatorConfig(device_capacity=20 * GIB))])
+    cof = (np.arange(16) % 3).astype(np.int32)
+    words = _native.wire_pack(reqs, offs)
+    assert words is not None
+    got, tl = _native.replay_host_wire(words, offs, cfgs, cof, True)
+    want, tl_ref = oracle.replay_batch(reqs, offs, cfgs, cof, timeline=True)
+    assert (got == want).all() and (tl == tl_ref).all()
+
+
+def test_wire_format_escalations_expand_for_wide_tiers():
+    # wire traces that leave the narrow pass (> 32 buckets of free blocks;
+    # > 2 TiB of segments) are expanded to pm_req_t for the wide tiers
+    holes = [alloc(i, i, 512) for i in range(3000)]
+    holes += [free(3000 + k, 2 * k) for k in range(1500)]
+    holes += [alloc(4500 + k, 3000 + k, 512) for k in range(700)]
+    big, k = [], 0
+    for i in range(200):
+        big.append(alloc(k, i, 12 * GIB + 513)); k += 1
+    assert _wire_ok(holes) and _wire_ok(big)
+    run_both([holes, big, [alloc(0, 0, 4096), free(1, 0)]],
+             [AllocatorConfig()] * 3)
 
 
 _WIDE_SCRIPT = r"""
