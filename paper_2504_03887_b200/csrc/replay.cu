@@ -52,7 +52,7 @@ Layout layout_for(int64_t total_events, int64_t max_trace_events,
   Layout L;
   size_t off = align_up(sizeof(pmb::Ctl), 256);
   L.retry_list = off;
-  off = align_up(off + 3 * sizeof(int32_t) * (size_t)(n_traces > 0 ? n_traces : 1),
+  off = align_up(off + 4 * sizeof(int32_t) * (size_t)(n_traces > 0 ? n_traces : 1),
                  256);
   const int64_t mx = max_trace_events > 0 ? max_trace_events : 1;
   L.nbmax_g = (int)(mx / 8 + 4);
@@ -74,6 +74,8 @@ struct Occupancy {
   int per_sm1 = 0;  // tier-1 retry kernel
   size_t smem1 = 0;
   int nbmax2 = 0;   // tier-2: one warp with a shared-memory directory
+  int nbmax3 = 0;   // tier-3: shared-memory directory over an HBM pool
+  size_t smem3 = 0;
   size_t smem2 = 0;
 };
 
@@ -169,10 +171,16 @@ int query_occupancy(Occupancy* out) {
     o.nbmax2 = (int)(((size_t)optin - 1024) / (kBucket_host * 24 + 32));
     while (o.nbmax2 > 8 && pmb::gmem_warp_bytes(o.nbmax2) > (size_t)optin) --o.nbmax2;
     o.smem2 = pmb::gmem_warp_bytes(o.nbmax2);
-    e = cudaFuncSetAttribute(pmb::replay_dirmem_kernel<1, true>,
+    e = cudaFuncSetAttribute(pmb::replay_dirmem_kernel<1, 0>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)o.smem2);
     if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute tier 2");
+    o.nbmax3 = (int)(((size_t)optin - 32 * 24 - 256) / 32);
+    o.smem3 = pmb::hybrid_smem_bytes(o.nbmax3);
+    e = cudaFuncSetAttribute(pmb::replay_dirmem_kernel<1, 1>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)o.smem3);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute tier 3");
     // load every replay kernel now (lazy module loading would otherwise
     // load a retry tier at its first launch, which waits for the device --
     // and pm_replay_host's main pass waits for copies enqueued after it)
@@ -183,8 +191,9 @@ int query_occupancy(Occupancy* out) {
           (const void*)pmn::replay_narrow_kernel<20>, (const void*)pmn::replay_narrow_kernel<24>,
           (const void*)pmb::replay_smem_kernel<8>, (const void*)pmb::replay_smem_kernel<12>,
           (const void*)pmb::replay_smem_kernel<14>, (const void*)pmb::replay_smem_kernel<16>,
-          (const void*)pmb::replay_dirmem_kernel<1, true>,
-          (const void*)pmb::replay_dirmem_kernel<kRetryWarps, false>};
+          (const void*)pmb::replay_dirmem_kernel<1, 0>,
+          (const void*)pmb::replay_dirmem_kernel<1, 1>,
+          (const void*)pmb::replay_dirmem_kernel<kRetryWarps, 2>};
       for (const void* f : fns) {
         e = cudaFuncGetAttributes(&fa, f);
         if (e != cudaSuccess) return cuda_fail(e, "cudaFuncGetAttributes");
@@ -217,6 +226,14 @@ void keep_pool_mapped() {
 }  // namespace
 
 extern "C" {
+
+#ifdef PM_STATS
+int pm_debug_stats(unsigned long long* out16) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out16, pmn::g_stats, 16 * sizeof(unsigned long long));
+  return 0;
+}
+#endif
 
 #ifdef PM_DEBUG_UNIFORM
 int pm_debug_nonuniform_line(void) {
@@ -342,18 +359,29 @@ int replay_batch_impl(const pm_req_t* reqs, const int64_t* trace_offsets,
     int32_t* list3 = retry_list + 2 * (size_t)n_traces;
     long long grid2 = occ.sms;
     if (n_traces < grid2) grid2 = n_traces;
-    pmb::replay_dirmem_kernel<1, true><<<(unsigned)grid2, 32, occ.smem2, stream>>>(
+    pmb::replay_dirmem_kernel<1, 0><<<(unsigned)grid2, 32, occ.smem2, stream>>>(
         reqs, trace_offsets, cfgs, cfg_of_trace, results, timeline, recs, ctl,
         2, list2, list3, nullptr, occ.nbmax2);
     e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "replay tier-2 launch");
-    pmb::replay_dirmem_kernel<kRetryWarps, false>
+    // tier 3: shared-memory directory, HBM entries (the per-warp pool fits
+    // in tier 4's region: nbmax3 is capped at tier 4's bucket count)
+    int32_t* list4 = retry_list + 3 * (size_t)n_traces;
+    const int nb3 = occ.nbmax3 < L.nbmax_g ? occ.nbmax3 : L.nbmax_g;
+    long long grid3 = L.retry_warps < occ.sms ? L.retry_warps : occ.sms;
+    pmb::replay_dirmem_kernel<1, 1><<<(unsigned)grid3, 32, pmb::hybrid_smem_bytes(nb3),
+                                      stream>>>(
+        reqs, trace_offsets, cfgs, cfg_of_trace, results, timeline, recs, ctl,
+        3, list3, list4, gpool, nb3);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "replay tier-3 launch");
+    pmb::replay_dirmem_kernel<kRetryWarps, 2>
         <<<L.retry_warps / kRetryWarps, kRetryWarps * 32, 0, stream>>>(
             reqs, trace_offsets, cfgs, cfg_of_trace, results, timeline, recs,
-            ctl, 3, list3, nullptr, gpool, L.nbmax_g);
+            ctl, 4, list4, nullptr, gpool, L.nbmax_g);
   }
   e = cudaGetLastError();
-  if (e != cudaSuccess) return cuda_fail(e, "replay tier-3 launch");
+  if (e != cudaSuccess) return cuda_fail(e, "replay tier-4 launch");
   return PM_SUCCESS;
 }
 

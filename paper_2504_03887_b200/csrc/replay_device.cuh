@@ -1023,9 +1023,9 @@ __device__ __forceinline__ void replay_trace(
 // ---- kernels -------------------------------------------------------------------
 
 struct Ctl {
-  unsigned work[4];   // work counters: main pass, tiers 1, 2 and 3
-  unsigned n_list[4]; // traces queued for tier 1 / 2 / 3 (index 1..3)
-  unsigned pad[56];
+  unsigned work[8];   // work counters: main pass, tiers 1..4
+  unsigned n_list[8]; // traces queued for tier k (index 1..4)
+  unsigned pad[48];
 };
 
 // Shared-memory layout of the main kernel (per CTA): the bucket pool
@@ -1118,14 +1118,26 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
   }
 }
 
-// Tiers 2 and 3 -- traces whose free blocks outgrew a dedicated 32-bucket
+// Tiers 2-4 -- traces whose free blocks outgrew a dedicated 32-bucket
 // register directory: the same replay with a memory-resident directory.
-// Tier 2 gives one warp a whole SM's shared memory (~290 buckets); tier 3
-// puts the entries and the directory in a per-warp HBM region sized for the
-// longest trace (free blocks never exceed live allocations + live segments
-// <= 2 x requests, and with every adjacent bucket pair holding > 32 entries
-// a directory of n/8+4 buckets always has room).
-template <int WARPS, bool SMEM>
+//   MODE 0 (tier 2): one warp owns a whole SM's shared memory (~290
+//           buckets), entries and directory both in shared memory;
+//   MODE 1 (tier 3): the directory (and the chunk staging) in shared
+//           memory, up to ~7k buckets, the entries in an HBM pool -- every
+//           directory search stays on-chip, only entry reads go to L2/HBM;
+//   MODE 2 (tier 4): everything in a per-warp HBM region sized for the
+//           longest trace (free blocks never exceed live allocations + live
+//           segments <= 2 x requests, and with every adjacent bucket pair
+//           holding > 32 entries a directory of n/8+4 buckets always has
+//           room).
+__host__ __device__ __forceinline__ size_t hybrid_smem_bytes(int nbmax) {
+  return 32 * 24 + (size_t)nbmax * 32;
+}
+__host__ __device__ __forceinline__ size_t hybrid_pool_bytes(int nbmax) {
+  return ((size_t)nbmax * kBucket * 24 + 255) / 256 * 256;
+}
+
+template <int WARPS, int MODE>
 __global__ void __launch_bounds__(WARPS * 32, 1)
     replay_dirmem_kernel(const pm_req_t* __restrict__ reqs,
                          const int64_t* __restrict__ offs,
@@ -1140,16 +1152,22 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
   const long long gw = (long long)blockIdx.x * WARPS + wib;
-  char* base = SMEM ? smem + (size_t)wib * gmem_warp_bytes(nbmax)
-                    : gpool + (size_t)gw * gmem_warp_bytes(nbmax);
   Pool P;
   Stage st;
-  carve_pool(base, nbmax, P);
-  carve_stage(base + (size_t)nbmax * kBucket * 24, st);
+  char* dbase;  // staging area followed by the directory arrays
+  if (MODE == 1) {
+    carve_pool(gpool + (size_t)gw * hybrid_pool_bytes(nbmax), nbmax, P);
+    dbase = smem + (size_t)wib * hybrid_smem_bytes(nbmax);
+  } else {
+    char* base = MODE == 0 ? smem + (size_t)wib * gmem_warp_bytes(nbmax)
+                           : gpool + (size_t)gw * gmem_warp_bytes(nbmax);
+    carve_pool(base, nbmax, P);
+    dbase = base + (size_t)nbmax * kBucket * 24;
+  }
+  carve_stage(dbase, st);
   DirMem dir;
   {
-    u64* q = reinterpret_cast<u64*>(base + (size_t)nbmax * kBucket * 24 +
-                                    32 * 24);
+    u64* q = reinterpret_cast<u64*>(dbase + 32 * 24);
     dir.dkey = q;
     dir.daddr = q + nbmax;
     int* ip = reinterpret_cast<int*>(q + 2 * (size_t)nbmax);

@@ -45,6 +45,17 @@ using pmb::lanemask_lt;
 using pmb::u32;
 using pmb::u64;
 
+#ifdef PM_STATS
+// debug build only (tools/stats_replay.py): pool-operation counters
+__device__ unsigned long long g_stats[16];
+#define PM_STAT(i) \
+  do {             \
+    if ((threadIdx.x & 31) == 0) atomicAdd(&g_stats[i], 1ull); \
+  } while (0)
+#else
+#define PM_STAT(i) ((void)0)
+#endif
+
 constexpr u32 kFreedU = 0xFFFFFFFFu;  // record size of a freed handle
 constexpr u32 kMaxU = 0xFFFFFFFEu;    // sizes / addresses stay below this
 
@@ -71,10 +82,14 @@ struct NRecs {
 };
 
 // Directory in registers: lane d holds bucket position d -- its lower bound
-// (packed ka), physical bucket and entry count.
+// (packed ka), physical bucket and occupancy mask (bit i: slot i holds an
+// entry).  Removing an entry clears its bit: entries never move between
+// slots except on bucket split / merge, so their ids stay valid and the
+// allocated neighbours' refs need no re-pointing.
 struct NDir {
   u64 db;
-  int dp, dc;
+  int dp;
+  unsigned dm;
   int nb;
   int lane;
   unsigned* cta_used;  // CTA-shared bitmap of physical buckets in use
@@ -83,7 +98,7 @@ struct NDir {
   __device__ __forceinline__ void init(int lane_) {
     db = ~0ull;
     dp = -1;
-    dc = 0;
+    dm = 0;
     nb = 0;
     lane = lane_;
   }
@@ -94,52 +109,55 @@ struct NDir {
   __device__ __forceinline__ int phys(int d) const {
     return __shfl_sync(kFull, dp, d);
   }
-  __device__ __forceinline__ int count(int d) const {
-    return __shfl_sync(kFull, dc, d);
+  __device__ __forceinline__ unsigned mask(int d) const {
+    return __shfl_sync(kFull, dm, d);
   }
-  __device__ __forceinline__ void add_count(int d, int delta) {
-    if (lane == d) dc += delta;
+  __device__ __forceinline__ void set_bit(int d, int b) {
+    if (lane == d) dm |= 1u << b;
   }
-  __device__ __forceinline__ void set_count(int d, int c) {
-    if (lane == d) dc = c;
+  __device__ __forceinline__ void clear_bit(int d, int b) {
+    if (lane == d) dm &= ~(1u << b);
+  }
+  __device__ __forceinline__ void set_mask(int d, unsigned m) {
+    if (lane == d) dm = m;
   }
   __device__ __forceinline__ int pos_of_phys(int p) const {
     return __ffs(__ballot_sync(kFull, dp == p)) - 1;
   }
   __device__ __forceinline__ int mergeable() const {
-    const int cn = __shfl_down_sync(kFull, dc, 1);
-    const unsigned m =
-        __ballot_sync(kFull, lane < nb - 1 && dc + cn <= kBucket);
+    const unsigned mn = __shfl_down_sync(kFull, dm, 1);
+    const unsigned m = __ballot_sync(
+        kFull, lane < nb - 1 && __popc(dm) + __popc(mn) <= kBucket);
     return m ? __ffs(m) - 1 : -1;
   }
-  __device__ __forceinline__ void insert(int d, u64 b, int p, int c) {
+  __device__ __forceinline__ void insert(int d, u64 b, int p, unsigned m) {
     const u64 ub = __shfl_up_sync(kFull, db, 1);
     const int up = __shfl_up_sync(kFull, dp, 1);
-    const int uc = __shfl_up_sync(kFull, dc, 1);
+    const unsigned um = __shfl_up_sync(kFull, dm, 1);
     if (lane > d) {
       db = ub;
       dp = up;
-      dc = uc;
+      dm = um;
     } else if (lane == d) {
       db = b;
       dp = p;
-      dc = c;
+      dm = m;
     }
     nb += 1;
   }
   __device__ __forceinline__ void erase(int d) {
     u64 nbd = __shfl_down_sync(kFull, db, 1);
     int np = __shfl_down_sync(kFull, dp, 1);
-    int nc = __shfl_down_sync(kFull, dc, 1);
+    unsigned nm = __shfl_down_sync(kFull, dm, 1);
     if (lane == 31) {
       nbd = ~0ull;
       np = -1;
-      nc = 0;
+      nm = 0;
     }
     if (lane >= d) {
       db = nbd;
       dp = np;
-      dc = nc;
+      dm = nm;
     }
     nb -= 1;
     if (d == 0 && lane == 0) db = 0;
@@ -214,13 +232,6 @@ __device__ __forceinline__ void set_link(const NRecs& rec, uint4* st, int hcmp,
   }
 }
 
-__device__ __forceinline__ void relink(const NRecs& rec, uint4* st, int hcmp,
-                                       int lane, u64 l, int id) {
-  const u32 L = lo(l), R = hi(l);
-  if (L != kNone) set_link(rec, st, hcmp, lane, L, 1, kFreeTag | (u32)id);
-  if (R != kNone) set_link(rec, st, hcmp, lane, R, 0, kFreeTag | (u32)id);
-}
-
 __device__ __forceinline__ void relink_lanes(const NRecs& rec, uint4* st,
                                              int hcmp, int lane, bool moved,
                                              u64 links, int dst) {
@@ -248,29 +259,37 @@ __device__ __forceinline__ int argmin_pk(bool valid, u64 x) {
   const unsigned any = __ballot_sync(kFull, valid);
   if (!any) return -1;
   if ((any & (any - 1)) == 0) return __ffs(any) - 1;
+  PM_STAT(10);
   const u32 mh = __reduce_min_sync(kFull, valid ? hi(x) : 0xffffffffu);
   const bool c = valid && hi(x) == mh;
   const unsigned bm = __ballot_sync(kFull, c);
   if ((bm & (bm - 1)) == 0) return __ffs(bm) - 1;
+  PM_STAT(11);
   const u32 ml = __reduce_min_sync(kFull, c ? lo(x) : 0xffffffffu);
   return __ffs(__ballot_sync(kFull, c && lo(x) == ml)) - 1;
 }
 
 // ---- bucket maintenance -----------------------------------------------------
 
+// Merge the first adjacent bucket pair whose entries fit in one bucket: the
+// right bucket's entries move into the left one's free slots.
 __device__ __forceinline__ bool try_merge(const NPool& P, NDir& dir,
                                           const NRecs& rec, uint4* st,
                                           int hcmp, int lane) {
   const int e = dir.mergeable();
   if (e < 0) return false;
+  PM_STAT(7);
   const int pa = dir.phys(e), pb = dir.phys(e + 1);
-  const int na = dir.count(e), nbb = dir.count(e + 1);
-  const bool mv = lane < nbb;
+  const unsigned ma = dir.mask(e), mb = dir.mask(e + 1);
+  const bool mv = (mb >> lane) & 1u;
   u64 ka = 0, l = 0;
-  const int src = pb * kBucket + lane, dst = pa * kBucket + na + lane;
+  int dst = -1;
   if (mv) {
-    ka = P.ka[src];
-    l = P.ln[src];
+    ka = P.ka[pb * kBucket + lane];
+    l = P.ln[pb * kBucket + lane];
+    // the r-th moving entry takes the r-th free slot of the left bucket
+    const int r = __popc(mb & lanemask_lt());
+    dst = pa * kBucket + (int)__fns(~ma, 0, r + 1);
   }
   __syncwarp();
   if (mv) {
@@ -279,13 +298,14 @@ __device__ __forceinline__ bool try_merge(const NPool& P, NDir& dir,
   }
   __syncwarp();
   relink_lanes(rec, st, hcmp, lane, mv, l, dst);
-  dir.set_count(e, na + nbb);
+  dir.set_mask(e, ma | __reduce_or_sync(kFull, mv ? 1u << (dst - pa * kBucket) : 0u));
   dir.erase(e + 1);
   dir.free_phys(pb);
   return true;
 }
 
-// Split the full bucket at position d into halves by ka rank.  False if no
+// Split the full bucket at position d: the upper half by ka rank moves to a
+// new bucket (slots 0..15), the lower half stays in place.  False if no
 // bucket can be had and nothing merges (overflow).
 __device__ __forceinline__ bool split_bucket(const NPool& P, NDir& dir, int d,
                                              const NRecs& rec, uint4* st,
@@ -297,87 +317,76 @@ __device__ __forceinline__ bool split_bucket(const NPool& P, NDir& dir, int d,
     q = dir.alloc_phys_wait();
     if (q < 0) return false;
   }
+  PM_STAT(6);
   const int p = dir.phys(d);
   const int base = p * kBucket;
-  const u64 ka = P.ka[base + lane];
+  const u64 ka = P.ka[base + lane];  // full bucket: every slot holds one
   const u64 l = P.ln[base + lane];
   int rank = 0;
 #pragma unroll 8
   for (int j = 0; j < kBucket; ++j)
     rank += __shfl_sync(kFull, ka, j) < ka ? 1 : 0;
   const bool up = rank >= kHalf;
-  const unsigned holes = __ballot_sync(kFull, up && lane < kHalf);
-  const unsigned movers = __ballot_sync(kFull, !up && lane >= kHalf);
-  int dst;
-  if (up) {
-    dst = q * kBucket + rank - kHalf;
-  } else if (lane >= kHalf) {
-    const int r = __popc(movers & lanemask_lt());
-    dst = base + (int)__fns(holes, 0, r + 1);
-  } else {
-    dst = base + lane;
-  }
   const int bl = __ffs(__ballot_sync(kFull, rank == kHalf)) - 1;
   const u64 bound = __shfl_sync(kFull, ka, bl);
+  const int dst = up ? q * kBucket + rank - kHalf : base + lane;
   __syncwarp();
-  P.ka[dst] = ka;
-  P.ln[dst] = l;
+  if (up) {
+    P.ka[dst] = ka;
+    P.ln[dst] = l;
+  }
   __syncwarp();
-  dir.set_count(d, kHalf);
-  dir.insert(d + 1, bound, q, kHalf);
-  relink_lanes(rec, st, hcmp, lane, dst != base + lane, l, dst);
+  dir.set_mask(d, ~__ballot_sync(kFull, up));
+  dir.insert(d + 1, bound, q, 0xFFFFu);
+  relink_lanes(rec, st, hcmp, lane, up, l, dst);
   return true;
 }
 
+// Insert a free block; returns its id or -1 on pool overflow.
 __device__ __forceinline__ int pool_insert(const NPool& P, NDir& dir, NCtx& c,
                                            u64 ka, u64 links, const NRecs& rec,
                                            uint4* st, int hcmp, int lane) {
   if (dir.nb == 0) {
     const int q = dir.alloc_phys_wait();
     if (q < 0) return -1;
-    dir.insert(0, 0ull, q, 0);
+    dir.insert(0, 0ull, q, 0u);
   }
   int d = dir.find(ka);
-  int cnt = dir.count(d);
-  while (cnt >= kBucket) {
+  unsigned m = dir.mask(d);
+  while (m == kFull) {
     if (!split_bucket(P, dir, d, rec, st, hcmp, lane)) return -1;
     d = dir.find(ka);
-    cnt = dir.count(d);
+    m = dir.mask(d);
   }
-  const int id = dir.phys(d) * kBucket + cnt;
+  const int slot = __ffs(~m) - 1;
+  const int id = dir.phys(d) * kBucket + slot;
+  PM_STAT(5);
   __syncwarp();
   P.ka[id] = ka;
   P.ln[id] = links;
-  dir.add_count(d, 1);
+  dir.set_bit(d, slot);
   c.F += 1;
   return id;
 }
 
-__device__ __forceinline__ int pool_remove(const NPool& P, NDir& dir, NCtx& c,
-                                           int id, const NRecs& rec, uint4* st,
-                                           int hcmp, int lane) {
+// Remove free block `id`: clear its slot (nothing moves); an emptied bucket
+// leaves the directory unless it is the last one.
+__device__ __forceinline__ void pool_remove(NDir& dir, NCtx& c, int id) {
   const int p = id / kBucket;
   const int d = dir.pos_of_phys(p);
-  const int last = dir.count(d) - 1;
-  const int lid = p * kBucket + last;
-  int moved = -1;
-  if (lid != id) {
-    const u64 lka = P.ka[lid], ll = P.ln[lid];
-    __syncwarp();
-    P.ka[id] = lka;
-    P.ln[id] = ll;
-    relink(rec, st, hcmp, lane, ll, id);
-    moved = lid;
-  }
-  dir.add_count(d, -1);
+  PM_STAT(2);
+  dir.clear_bit(d, id % kBucket);
   c.F -= 1;
-  if (last == 0 && dir.nb > 1) {
+  if (dir.mask(d) == 0u && dir.nb > 1) {
+    PM_STAT(4);
     dir.erase(d);
     dir.free_phys(p);
   }
-  return moved;
 }
 
+// Rekey entry `id` to (ka, links) -- in place when it stays in its bucket
+// -- or, with id < 0, insert a new entry.  Returns the entry's id (-1 on
+// overflow); the caller re-points the neighbours whose refs changed.
 __device__ __forceinline__ int pool_upsert(const NPool& P, NDir& dir, NCtx& c,
                                            int id, u64 ka, u64 links,
                                            const NRecs& rec, uint4* st,
@@ -385,44 +394,43 @@ __device__ __forceinline__ int pool_upsert(const NPool& P, NDir& dir, NCtx& c,
   if (id >= 0) {
     const int d = dir.find(ka);
     if (dir.phys(d) == id / kBucket) {
+      PM_STAT(0);
       __syncwarp();
       P.ka[id] = ka;
       P.ln[id] = links;
       return id;
     }
-    pool_remove(P, dir, c, id, rec, st, hcmp, lane);
+    PM_STAT(1);
+    pool_remove(dir, c, id);
   }
   return pool_insert(P, dir, c, ka, links, rec, st, hcmp, lane);
 }
 
 // Best fit (allocator.py:203-221): argmin ka over entries
 // with ru <= size_u and size_u - ru < span (span 0xFFFFFFFF: no bound --
-// size_u - ru <= kMaxU - 1 always).
+// size_u - ru <= kMaxU - 1 always).  The bucket holding ru and the next
+// one are loaded together; the next one's minimum is the only candidate
+// when the first holds none.
 __device__ __forceinline__ int best_fit(const NPool& P, const NDir& dir,
                                         u32 ru, u32 span, int lane) {
   if (dir.nb == 0) return -1;
   const int d = dir.find((u64)ru << 32);
-  {
-    const int p = dir.phys(d);
-    const int id = p * kBucket + lane;
-    const bool in = lane < dir.count(d);
-    const u64 ka = in ? P.ka[id] : ~0ull;
-    const bool el = in && hi(ka) >= ru && hi(ka) - ru < span;
-    const int w = argmin_pk(el, ka);
-    if (w >= 0) return p * kBucket + w;
-  }
-  if (d + 1 < dir.nb) {
-    // every entry of the next bucket is larger: its minimum is the only
-    // remaining candidate
-    const int p = dir.phys(d + 1);
-    const int id = p * kBucket + lane;
-    const bool in = lane < dir.count(d + 1);
-    const u64 ka = in ? P.ka[id] : ~0ull;
-    const int w = argmin_pk(in, ka);
-    if (w >= 0) {
-      const u64 kw = __shfl_sync(kFull, ka, w);
-      if (hi(kw) - ru < span) return p * kBucket + w;
-    }
+  const int p = dir.phys(d);
+  const bool in = (dir.mask(d) >> lane) & 1u;
+  const bool has_next = d + 1 < dir.nb;
+  const int p2 = dir.phys(d + 1);
+  const bool in2 = has_next && ((dir.mask(d + 1) >> lane) & 1u);
+  const u64 ka = in ? P.ka[p * kBucket + lane] : ~0ull;
+  const u64 ka2 = in2 ? P.ka[p2 * kBucket + lane] : ~0ull;
+  PM_STAT(8);
+  const bool el = in && hi(ka) >= ru && hi(ka) - ru < span;
+  const int w = argmin_pk(el, ka);
+  if (w >= 0) return p * kBucket + w;
+  PM_STAT(9);
+  const int w2 = argmin_pk(in2, ka2);
+  if (w2 >= 0) {
+    const u64 kw = __shfl_sync(kFull, ka2, w2);
+    if (hi(kw) - ru < span) return p2 * kBucket + w2;
   }
   return -1;
 }
@@ -437,7 +445,7 @@ __device__ __forceinline__ int find_release_candidate(const NPool& P,
   for (int d = 0; d < dir.nb; ++d) {
     const int p = dir.phys(d);
     const int id = p * kBucket + lane;
-    if (lane < dir.count(d) && P.ln[id] == ~0ull) {
+    if (((dir.mask(d) >> lane) & 1u) && P.ln[id] == ~0ull) {
       const u64 ka = P.ka[id];
       if ((long long)hi(ka) > thr) {
         const u64 key = pk(0xFFFFFFFFu - hi(ka), lo(ka));
@@ -481,7 +489,7 @@ __device__ __forceinline__ void make_room(const NPool& P, NDir& dir, NCtx& c,
       continue;
     }
     const long long sz = (long long)hi(P.ka[id]) << cf.s;
-    pool_remove(P, dir, c, id, rec, st, hcmp, lane);
+    pool_remove(dir, c, id);
     c.reserved -= sz;
     c.nseg -= 1;
   }
@@ -687,6 +695,9 @@ __device__ __forceinline__ void replay_trace(
         u32 f1 = kNone, f2 = kNone;
         int both_pid = -1;
         u32 both_S = 0, both_rS = 0, both_rR = kNone;
+        // neighbour refs that must name the upserted entry even when it
+        // keeps its id (the other side is re-pointed only if it moved)
+        bool newL = false, newR = false;
         const bool is_alloc = kind == PM_KIND_ALLOC;
         bool split_out = false;
         u32 out_a = 0, out_s = 0, out_L = kNone, out_R = kNone;
@@ -775,11 +786,13 @@ __device__ __forceinline__ void replay_trace(
               up_id = pid;
               up_ka = P.ka[pid] + ((u64)S << 32);
               up_l = pmb::mk_links(lo(P.ln[pid]), R);
+              newR = true;
             } else if (!lf && rf) {
               const int rid = (int)(R & ~kFreeTag);
               up_id = rid;
               up_ka = pk(hi(P.ka[rid]) + S, A);
               up_l = pmb::mk_links(L, hi(P.ln[rid]));
+              newL = true;
             } else {
               const int rid = (int)(R & ~kFreeTag);
               both_pid = (int)(L & ~kFreeTag);
@@ -792,12 +805,12 @@ __device__ __forceinline__ void replay_trace(
         }
         if (sts == PM_OK) {
           if (rm_id >= 0) {
-            const int moved = pool_remove(P, dir, c, rm_id, rec, st, hcmp, lane);
+            pool_remove(dir, c, rm_id);
             if (both_pid >= 0) {
-              const int pid = moved == both_pid ? rm_id : both_pid;
-              up_id = pid;
-              up_ka = P.ka[pid] + ((u64)(both_S + both_rS) << 32);
-              up_l = pmb::mk_links(lo(P.ln[pid]), both_rR);
+              up_id = both_pid;
+              up_ka = P.ka[both_pid] + ((u64)(both_S + both_rS) << 32);
+              up_l = pmb::mk_links(lo(P.ln[both_pid]), both_rR);
+              newR = true;
             }
           }
           if (up) {
@@ -810,7 +823,12 @@ __device__ __forceinline__ void replay_trace(
             if (nid < 0) {
               sts = PM_POOL_OVERFLOW;
             } else {
-              relink(rec, st, hcmp, lane, up_l, nid);
+              const bool moved = nid != up_id;
+              const u32 L = lo(up_l), R = hi(up_l);
+              if ((newL || moved) && L != kNone)
+                set_link(rec, st, hcmp, lane, L, 1, kFreeTag | (u32)nid);
+              if ((newR || moved) && R != kNone)
+                set_link(rec, st, hcmp, lane, R, 0, kFreeTag | (u32)nid);
               if (split_out) out_R = kFreeTag | (u32)nid;
             }
           }

@@ -79,6 +79,12 @@ class DeviceBatch:
             self.total_events, self.max_trace_events,
             ctypes.c_void_p(s.cuda_stream)), self.lib)
 
+    def tier_counts(self) -> list[int]:
+        """Traces the last launch handed to retry tiers 1-4 (diagnostic:
+        the workspace's control block, csrc/replay_device.cuh Ctl)."""
+        ctl = self.d_ws[:64].cpu().numpy().view(np.uint32)
+        return [int(x) for x in ctl[9:13]]
+
     def results(self) -> np.ndarray:
         self.torch.cuda.synchronize(self.device)
         return self.d_results.cpu().numpy().view(RESULT_DTYPE).copy()

@@ -330,7 +330,7 @@ def test_many_traces_per_warp_vs_oracle(monkeypatch):
 
 def test_hbm_tier_vs_oracle():
     # 10k non-adjacent free blocks outgrow the shared-memory tiers (~9k
-    # entries) and land in the HBM-directory tier
+    # entries) and land in tier 3 (shared-memory directory, HBM entries)
     seq = [alloc(i, i, 512) for i in range(20_000)]
     seq += [free(20_000 + k, 2 * k) for k in range(10_000)]
     seq += [alloc(30_000 + k, 50_000 + k, 512) for k in range(3_000)]
@@ -343,3 +343,29 @@ def test_hbm_tier_vs_oracle():
     assert int(want[0]["max_free_blocks"]) >= 10_000
     assert_same(got, want)
     assert (tl == tl_ref).all()
+
+
+def _holes(n_holes, fill):
+    seq = [alloc(i, i, 512) for i in range(2 * n_holes)]
+    seq += [free(2 * n_holes + k, 2 * k) for k in range(n_holes)]
+    seq += [alloc(3 * n_holes + k, 10 * n_holes + k, 512) for k in range(fill)]
+    return seq
+
+
+def test_retry_tiers_3_and_4_vs_oracle():
+    # 20k holes stay in tier 3; 240k holes outgrow its ~7k-bucket shared
+    # directory and finish in tier 4 (everything in HBM)
+    traces = [_holes(20_000, 2_000), _holes(240_000, 3_000)]
+    packed = [pack_trace(t) for t in traces]
+    offs = np.zeros(3, dtype=np.int64)
+    np.cumsum([len(p.reqs) for p in packed], out=offs[1:])
+    reqs = np.concatenate([p.reqs for p in packed])
+    cfg = cfg_record(AllocatorConfig())
+    batch = DeviceBatch(reqs, offs, cfg)
+    batch.launch()
+    got = batch.results()
+    tiers = batch.tier_counts()
+    want, _ = oracle.replay_batch(reqs, offs, cfg)
+    assert_same(got, want)
+    assert int(want[1]["max_free_blocks"]) >= 240_000
+    assert tiers[2] == 2 and tiers[3] == 1, tiers  # both reach tier 3, one tier 4

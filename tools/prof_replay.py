@@ -36,8 +36,8 @@ def main():
         dt = time.perf_counter() - t0
         res = batch.results()
         ev = int(res["n_events_replayed"].sum())
-        ctl = batch.d_ws[:32].cpu().numpy().view(np.uint32)
-        print(f"tier-1 {ctl[5]}, tier-2 {ctl[6]}, tier-3 {ctl[7]} retries")
+        ctl = batch.d_ws[:64].cpu().numpy().view(np.uint32)
+        print(f"tier-1 {ctl[9]}, tier-2 {ctl[10]}, tier-3 {ctl[11]}, tier-4 {ctl[12]} retries")
         print(f"{args.traces} traces {ev} events {dt*1e3:.1f} ms "
               f"{ev/dt/1e9:.3f} Gev/s maxF {res['max_free_blocks'].max()} "
               f"status {set(res['status'].tolist())}")
