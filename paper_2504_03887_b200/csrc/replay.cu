@@ -33,7 +33,7 @@ int cuda_fail(cudaError_t e, const char* where) {
 }
 
 constexpr int kWarps = 12;        // wide main kernel (PM_REPLAY_WIDE=1)
-constexpr int kNarrowWarps = 20;  // narrow main kernel (PM_REPLAY_WARPS: 12, 16, 20, 24)
+constexpr int kNarrowWarps = 24;  // narrow main kernel (PM_REPLAY_WARPS: 12..32)
 constexpr size_t kBucket_host = 32;  // warps (traces in flight) per CTA, 1 CTA / SM
 constexpr int kRetryWarps = 1;
 constexpr int kMaxRetryWarps = 64;
@@ -151,6 +151,10 @@ int query_occupancy(Occupancy* out) {
         rc = setup_narrow<20>(optin, cap, &o.buckets, &o.smem, &o.per_sm);
       else if (o.warps == 24)
         rc = setup_narrow<24>(optin, cap, &o.buckets, &o.smem, &o.per_sm);
+      else if (o.warps == 28)
+        rc = setup_narrow<28>(optin, cap, &o.buckets, &o.smem, &o.per_sm);
+      else if (o.warps == 32)
+        rc = setup_narrow<32>(optin, cap, &o.buckets, &o.smem, &o.per_sm);
       else {
         o.warps = 16;
         rc = setup_narrow<16>(optin, cap, &o.buckets, &o.smem, &o.per_sm);
@@ -189,6 +193,7 @@ int query_occupancy(Occupancy* out) {
       const void* fns[] = {
           (const void*)pmn::replay_narrow_kernel<12>, (const void*)pmn::replay_narrow_kernel<16>,
           (const void*)pmn::replay_narrow_kernel<20>, (const void*)pmn::replay_narrow_kernel<24>,
+          (const void*)pmn::replay_narrow_kernel<28>, (const void*)pmn::replay_narrow_kernel<32>,
           (const void*)pmb::replay_smem_kernel<8>, (const void*)pmb::replay_smem_kernel<12>,
           (const void*)pmb::replay_smem_kernel<14>, (const void*)pmb::replay_smem_kernel<16>,
           (const void*)pmb::replay_dirmem_kernel<1, 0>,
@@ -326,6 +331,10 @@ int replay_batch_impl(const pm_req_t* reqs, const int64_t* trace_offsets,
       PM_LAUNCH_NARROW(20);
     else if (occ.warps == 24)
       PM_LAUNCH_NARROW(24);
+    else if (occ.warps == 28)
+      PM_LAUNCH_NARROW(28);
+    else if (occ.warps == 32)
+      PM_LAUNCH_NARROW(32);
     else
       PM_LAUNCH_NARROW(16);
   } else if (occ.warps == 12)

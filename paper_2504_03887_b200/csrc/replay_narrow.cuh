@@ -214,9 +214,22 @@ struct NDir {
 };
 
 struct NCtx {
-  long long reserved, allocated, peak_reserved, peak_allocated;
+  long long reserved, allocated, peak_allocated;
+  int F, maxF;
+};
+
+// Per-trace values read only on the allocation / segment paths live in the
+// warp's shared staging area rather than in registers (registers set how
+// many warps fit per SM).
+struct NWarpState {
+  const pm_cfg_t* cp;
+  u32 amask;      // alignment - 1 (bytes; alignment <= 2^31 in this pass)
+  u32 lim;        // largest rounded request in units (0: unit too large)
+  u32 span;       // best-fit window in units (0xFFFFFFFF: unbounded)
+  u32 split_lim;  // splittable iff size_u <= split_lim
+  long long peak_reserved;
   u32 next_base;  // units
-  int F, maxF, nseg, nseg_peak;
+  int nseg, nseg_peak, pad;
 };
 
 // ---- record refs (global store + staged mirror) ---------------------------
@@ -460,23 +473,14 @@ __device__ __forceinline__ int find_release_candidate(const NPool& P,
   return w < 0 ? -1 : __shfl_sync(kFull, bid, w);
 }
 
-struct NCfg {
-  const pm_cfg_t* cp;
-  u32 amask;     // alignment - 1 (bytes; alignment <= 2^31 in this pass)
-  u32 span;      // best-fit window in units (0xFFFFFFFF: unbounded)
-  u32 split_lim; // splittable iff size_u <= split_lim
-  u32 lim;       // largest rounded request in units (0: unit too large)
-  int s;         // unit shift
-};
-
 __device__ __forceinline__ void make_room(const NPool& P, NDir& dir, NCtx& c,
-                                          long long seg, const NCfg& cf,
+                                          long long seg, NWarpState* ws, int s,
                                           const NRecs& rec, uint4* st,
                                           int hcmp, int lane) {
-  const long long capacity = cf.cp->device_capacity;
-  const long long t = cf.cp->max_split_size;
+  const long long capacity = ws->cp->device_capacity;
+  const long long t = ws->cp->max_split_size;
   // stage-1 threshold in units: size > t  <=>  size_u > floor(t / u)
-  const long long rel_thr = t >= 0 ? (long long)((u64)t >> cf.s) : -1;
+  const long long rel_thr = t >= 0 ? (long long)((u64)t >> s) : -1;
   int stage = t >= 0 ? 1 : 2;
   if (stage == 2 && c.reserved + seg <= capacity) return;
   for (;;) {
@@ -488,10 +492,12 @@ __device__ __forceinline__ void make_room(const NPool& P, NDir& dir, NCtx& c,
       stage = 2;
       continue;
     }
-    const long long sz = (long long)hi(P.ka[id]) << cf.s;
+    const long long sz = (long long)hi(P.ka[id]) << s;
     pool_remove(dir, c, id);
     c.reserved -= sz;
-    c.nseg -= 1;
+    __syncwarp();
+    ws->nseg -= 1;  // uniform store
+    __syncwarp();
   }
 }
 
@@ -542,6 +548,7 @@ struct NStage {
   ulonglong2* buf;  // [2][32]
   u64* bar;         // [2]
   uint4* rec;       // [32]
+  NWarpState* ws;
   u32 g;            // chunks consumed by this warp (buffer g & 1)
 };
 
@@ -560,32 +567,40 @@ __device__ __forceinline__ void replay_trace(
   const long long e0 = offs[tr];
   const int n = (int)(offs[tr + 1] - e0);  // < 2^31 (pm_replay_batch)
   const pm_cfg_t* cp = cfgs + (cfg_of ? cfg_of[tr] : 0);
-  NCfg cf;
-  cf.cp = cp;
-  cf.amask = (u32)(cp->alignment - 1);
+  NWarpState* ws = sg.ws;
+  int s;
   {
-    int s = ctz64(cp->alignment);
+    s = ctz64(cp->alignment);
     s = min(s, ctz64(cp->k_small_buffer));
     s = min(s, ctz64(cp->k_large_buffer));
     s = min(s, ctz64(cp->k_round_large));
-    cf.s = s;
-  }
-  const int s = cf.s;
-  // units above 16 MiB are left to the wide tiers altogether
-  cf.lim = s > 24 || cp->alignment > (1ll << 31) ? 0u : kMaxU;
-  {
     const long long t = cp->max_split_size;
+    u32 span, split_lim;
     if (t >= 0) {
       const u64 sp = ((u64)t + ((1ull << s) - 1)) >> s;  // ceil(t / u)
-      cf.span = sp > 0xFFFFFFFEull ? 0xFFFFFFFFu : (u32)sp;
+      span = sp > 0xFFFFFFFEull ? 0xFFFFFFFFu : (u32)sp;
       const u64 fl = (u64)t >> s;
-      cf.split_lim = fl > 0xFFFFFFFFull ? 0xFFFFFFFFu : (u32)fl;
+      split_lim = fl > 0xFFFFFFFFull ? 0xFFFFFFFFu : (u32)fl;
     } else {
-      cf.span = 0xFFFFFFFFu;
-      cf.split_lim = 0xFFFFFFFFu;
+      span = 0xFFFFFFFFu;
+      split_lim = 0xFFFFFFFFu;
     }
+    __syncwarp();
+    if (lane == 0) {
+      NWarpState w;
+      w.cp = cp;
+      w.amask = (u32)(cp->alignment - 1);
+      // units above 16 MiB are left to the wide tiers altogether
+      w.lim = s > 24 || cp->alignment > (1ll << 31) ? 0u : kMaxU;
+      w.span = span;
+      w.split_lim = split_lim;
+      w.peak_reserved = 0;
+      w.next_base = 0;
+      w.nseg = w.nseg_peak = w.pad = 0;
+      *ws = w;
+    }
+    __syncwarp();
   }
-  const u64 amask = cf.amask;  // widened at use
 
   NRecs rec;
   rec.base = rec_base + 4 * (size_t)e0;
@@ -597,9 +612,8 @@ __device__ __forceinline__ void replay_trace(
   __syncwarp();
 
   NCtx c;
-  c.reserved = c.allocated = c.peak_reserved = c.peak_allocated = 0;
-  c.next_base = 0;
-  c.F = c.maxF = c.nseg = c.nseg_peak = 0;
+  c.reserved = c.allocated = c.peak_allocated = 0;
+  c.F = c.maxF = 0;
   int status = PM_OK;
   int stop = -1;
 
@@ -707,11 +721,13 @@ __device__ __forceinline__ void replay_trace(
           } else if (size <= 0) {
             sts = PM_ZERO_SIZE;
           } else if ((ks >> 2) != 0u ||
-                     ((((u64)size + amask) & ~amask) >> s) > (u64)cf.lim) {
+                     ((((u64)size + ws->amask) & ~(u64)ws->amask) >> s) >
+                         (u64)ws->lim) {
             sts = PM_POOL_OVERFLOW;  // outside the encoding: wide tiers
           } else {
-            const u32 ru = (u32)((((u64)size + amask) & ~amask) >> s);
-            const int id = best_fit(P, dir, ru, cf.span, lane);
+            const u32 ru = (u32)((((u64)size + ws->amask) & ~(u64)ws->amask) >> s);
+            const u32 split_lim = ws->split_lim;
+            const int id = best_fit(P, dir, ru, ws->span, lane);
             if (id >= 0) {
               // hit: _take (allocator.py:234-242), _split (:223-232)
               const u64 KA = P.ka[id];
@@ -721,7 +737,7 @@ __device__ __forceinline__ void replay_trace(
               out_a = A;
               out_L = Lf;
               f1 = Lf;
-              if (S <= cf.split_lim && S > ru) {
+              if (S <= split_lim && S > ru) {
                 up = true;
                 up_id = id;
                 up_ka = pk(S - ru, A + ru);
@@ -737,25 +753,33 @@ __device__ __forceinline__ void replay_trace(
             } else {
               // miss: new segment (allocator.py:278-288, 244-250)
               pmb::Cfg wc;
-              wc.cp = cp;
+              wc.cp = ws->cp;
               const long long seg =
                   pmb::segment_size_for((long long)ru << s, wc);
-              const long long capacity = cp->device_capacity;
+              const long long capacity = wc.cp->device_capacity;
               if (capacity >= 0 && c.reserved + seg > capacity) {
-                make_room(P, dir, c, seg, cf, rec, st, hcmp, lane);
+                make_room(P, dir, c, seg, ws, s, rec, st, hcmp, lane);
                 if (c.reserved + seg > capacity) sts = PM_OOM;
               }
               const u64 seg_u = (u64)seg >> s;
-              if (sts == PM_OK && (u64)c.next_base + seg_u > kMaxU)
+              const u32 A = ws->next_base;
+              if (sts == PM_OK && (u64)A + seg_u > kMaxU)
                 sts = PM_POOL_OVERFLOW;
               if (sts == PM_OK) {
-                const u32 A = c.next_base;
-                c.next_base += (u32)seg_u;
                 c.reserved += seg;
-                c.nseg += 1;
-                c.nseg_peak = max(c.nseg_peak, c.nseg);
+                {
+                  const int ns = ws->nseg + 1;
+                  const int np = max(ws->nseg_peak, ns);
+                  const long long pr = max(ws->peak_reserved, c.reserved);
+                  __syncwarp();
+                  ws->next_base = A + (u32)seg_u;  // uniform stores
+                  ws->nseg = ns;
+                  ws->nseg_peak = np;
+                  ws->peak_reserved = pr;  // reserved grows only here
+                  __syncwarp();
+                }
                 out_a = A;
-                if ((u32)seg_u <= cf.split_lim && (u32)seg_u > ru) {
+                if ((u32)seg_u <= split_lim && (u32)seg_u > ru) {
                   up = true;
                   up_ka = pk((u32)seg_u - ru, A + ru);
                   up_l = pmb::mk_links(kNone, kNone);
@@ -840,7 +864,6 @@ __device__ __forceinline__ void replay_trace(
           __syncwarp();
           if (is_alloc) {
             c.allocated += (long long)out_s << s;
-            c.peak_reserved = max(c.peak_reserved, c.reserved);
             c.peak_allocated = max(c.peak_allocated, c.allocated);
             if (lane == j) {
               const uint4 o = make_uint4(out_a, out_s, out_L, out_R);
@@ -907,7 +930,7 @@ __device__ __forceinline__ void replay_trace(
   dir.release_all();
   if (lane == 0) {
     pm_result_t res;
-    res.peak_reserved = c.peak_reserved;
+    res.peak_reserved = ws->peak_reserved;
     res.peak_allocated = c.peak_allocated;
     res.final_reserved = c.reserved;
     res.final_allocated = c.allocated;
@@ -915,8 +938,8 @@ __device__ __forceinline__ void replay_trace(
     res.n_events_replayed =
         status == PM_OK ? n : (status == PM_OOM ? stop + 1 : stop);
     res.status = status;
-    res.n_segments_final = c.nseg;
-    res.n_segments_peak = c.nseg_peak;
+    res.n_segments_final = ws->nseg;
+    res.n_segments_peak = ws->nseg_peak;
     res.max_free_blocks = c.maxF;
     results[tr] = res;
   }
@@ -925,7 +948,7 @@ __device__ __forceinline__ void replay_trace(
 // Shared memory per CTA: the pool (B x 32 x 16 B), per warp a staging area
 // (two 512 B request buffers, 512 B of gathered records, two barriers),
 // and the pool's in-use bitmap.
-constexpr size_t kWarpStageBytes = 2 * 32 * 16 + 32 * 16 + 16;
+constexpr size_t kWarpStageBytes = 2 * 32 * 16 + 32 * 16 + 16 + sizeof(NWarpState);
 __host__ __device__ __forceinline__ size_t smem_cta_bytes(int buckets,
                                                           int warps) {
   return (size_t)buckets * kBucket * 16 + (size_t)warps * kWarpStageBytes +
@@ -960,6 +983,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
   sg.buf = reinterpret_cast<ulonglong2*>(wst);
   sg.rec = reinterpret_cast<uint4*>(wst + 2 * 32 * 16);
   sg.bar = reinterpret_cast<u64*>(wst + 3 * 32 * 16);
+  sg.ws = reinterpret_cast<NWarpState*>(wst + 3 * 32 * 16 + 16);
   sg.g = 0;
   unsigned* used = reinterpret_cast<unsigned*>(smem + E * 16 +
                                                (size_t)WARPS * kWarpStageBytes);

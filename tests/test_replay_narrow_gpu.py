@@ -215,7 +215,8 @@ print("wide ok")
 
 @pytest.mark.parametrize("env", [{"PM_REPLAY_WIDE": "1"},
                                  {"PM_REPLAY_WARPS": "12"},
-                                 {"PM_REPLAY_WARPS": "20"}])
+                                 {"PM_REPLAY_WARPS": "20"},
+                                 {"PM_REPLAY_WARPS": "32"}])
 def test_main_kernel_variants_vs_oracle(env):
     # the wide main kernel (PM_REPLAY_WIDE=1) and the other narrow widths;
     # the launch configuration is fixed per process, hence a subprocess
