@@ -182,10 +182,11 @@ struct NDir {
     return __shfl_sync(kFull, p, 0);
   }
   // The CTA's pool is exhausted: wait for another warp to hand a bucket
-  // back (buckets empty out continuously as free blocks are taken), unless
-  // every warp replaying a trace in this CTA is itself waiting -- then -1
-  // (the trace escalates to the wide tiers).  ctr[0] waiting warps, ctr[1]
-  // active warps, after the bitmap.
+  // back (buckets empty out continuously as free blocks are taken).  If
+  // every warp replaying a trace in this CTA is waiting, ONE of them (the
+  // holder of the victim token) returns -1: its trace escalates to the wide
+  // tiers and its buckets go back to the others.  ctr[0] waiting warps,
+  // ctr[1] active warps, ctr[2] victim token, after the bitmap.
   __device__ __forceinline__ int alloc_phys_wait() {
     int p = alloc_phys();
     if (p >= 0) return p;
@@ -195,13 +196,19 @@ struct NDir {
       __nanosleep(500);
       p = alloc_phys();
       if (p >= 0) break;
-      int stuck = 0;
-      if (lane == 0)
-        stuck = *(volatile int*)&ctr[0] >= *(volatile int*)&ctr[1];
-      if (__shfl_sync(kFull, stuck, 0)) break;
+      int victim = 0;
+      if (lane == 0 &&
+          *(volatile int*)&ctr[0] >= *(volatile int*)&ctr[1])
+        victim = atomicCAS(&ctr[2], 0, 1) == 0;
+      if (__shfl_sync(kFull, victim, 0)) break;
     }
     if (lane == 0) atomicSub(&ctr[0], 1);
     return p;
+  }
+  // a victim hands its token back once its buckets are released
+  __device__ __forceinline__ void release_victim_token() {
+    int* ctr = reinterpret_cast<int*>(cta_used + cta_words);
+    if (lane == 0) atomicExch(&ctr[2], 0);
   }
   __device__ __forceinline__ void free_phys(int p) {
     if (lane == 0) atomicAnd(&cta_used[p >> 5], ~(1u << (p & 31)));
@@ -213,9 +220,11 @@ struct NDir {
   __device__ __forceinline__ bool full() const { return nb >= 32; }
 };
 
+struct NWarpState;
 struct NCtx {
-  long long reserved, allocated, peak_allocated;
-  int F, maxF;
+  long long reserved, allocated;
+  int F;
+  NWarpState* ws;
 };
 
 // Per-trace values read only on the allocation / segment paths live in the
@@ -227,9 +236,9 @@ struct NWarpState {
   u32 lim;        // largest rounded request in units (0: unit too large)
   u32 span;       // best-fit window in units (0xFFFFFFFF: unbounded)
   u32 split_lim;  // splittable iff size_u <= split_lim
-  long long peak_reserved;
+  long long peak_reserved, peak_allocated;
   u32 next_base;  // units
-  int nseg, nseg_peak, pad;
+  int nseg, nseg_peak, maxF;  // maxF: free-block high-water mark
 };
 
 // ---- record refs (global store + staged mirror) ---------------------------
@@ -374,11 +383,13 @@ __device__ __forceinline__ int pool_insert(const NPool& P, NDir& dir, NCtx& c,
   const int slot = __ffs(~m) - 1;
   const int id = dir.phys(d) * kBucket + slot;
   PM_STAT(5);
+  c.F += 1;
+  const int mf = max(c.ws->maxF, c.F);  // the count grows only here
   __syncwarp();
   P.ka[id] = ka;
   P.ln[id] = links;
+  c.ws->maxF = mf;  // uniform stores
   dir.set_bit(d, slot);
-  c.F += 1;
   return id;
 }
 
@@ -594,9 +605,9 @@ __device__ __forceinline__ void replay_trace(
       w.lim = s > 24 || cp->alignment > (1ll << 31) ? 0u : kMaxU;
       w.span = span;
       w.split_lim = split_lim;
-      w.peak_reserved = 0;
+      w.peak_reserved = w.peak_allocated = 0;
       w.next_base = 0;
-      w.nseg = w.nseg_peak = w.pad = 0;
+      w.nseg = w.nseg_peak = w.maxF = 0;
       *ws = w;
     }
     __syncwarp();
@@ -612,8 +623,9 @@ __device__ __forceinline__ void replay_trace(
   __syncwarp();
 
   NCtx c;
-  c.reserved = c.allocated = c.peak_allocated = 0;
-  c.F = c.maxF = 0;
+  c.reserved = c.allocated = 0;
+  c.F = 0;
+  c.ws = ws;
   int status = PM_OK;
   int stop = -1;
 
@@ -684,11 +696,8 @@ __device__ __forceinline__ void replay_trace(
     const int hcmp = hok ? my_h : -1;
     __syncwarp();
 
-    ulonglong2 ev_next = cb[0];
     for (int j = 0; j < cnt; ++j) {
-      // the next request's load is issued before this one's dependent chain
-      const ulonglong2 ev = ev_next;
-      if (j + 1 < cnt) ev_next = cb[j + 1];
+      const ulonglong2 ev = cb[j];
       const long long size = (long long)ev.x;
       const int hj = (int)lo(ev.y);
       const unsigned ks = hi(ev.y);
@@ -860,11 +869,12 @@ __device__ __forceinline__ void replay_trace(
         if (sts == PM_OK) {
           if (f2 != kNone) set_link(rec, st, hcmp, lane, f2, 0, (u32)hj);
           if (f1 != kNone) set_link(rec, st, hcmp, lane, f1, 1, (u32)hj);
-          c.maxF = max(c.maxF, c.F);
           __syncwarp();
           if (is_alloc) {
             c.allocated += (long long)out_s << s;
-            c.peak_allocated = max(c.peak_allocated, c.allocated);
+            const long long pa = max(ws->peak_allocated, c.allocated);
+            __syncwarp();
+            ws->peak_allocated = pa;  // uniform store
             if (lane == j) {
               const uint4 o = make_uint4(out_a, out_s, out_L, out_R);
               st[j] = o;
@@ -931,7 +941,7 @@ __device__ __forceinline__ void replay_trace(
   if (lane == 0) {
     pm_result_t res;
     res.peak_reserved = ws->peak_reserved;
-    res.peak_allocated = c.peak_allocated;
+    res.peak_allocated = ws->peak_allocated;
     res.final_reserved = c.reserved;
     res.final_allocated = c.allocated;
     res.stop_index = stop;
@@ -940,7 +950,7 @@ __device__ __forceinline__ void replay_trace(
     res.status = status;
     res.n_segments_final = ws->nseg;
     res.n_segments_peak = ws->nseg_peak;
-    res.max_free_blocks = c.maxF;
+    res.max_free_blocks = ws->maxF;
     results[tr] = res;
   }
 }
@@ -948,11 +958,13 @@ __device__ __forceinline__ void replay_trace(
 // Shared memory per CTA: the pool (B x 32 x 16 B), per warp a staging area
 // (two 512 B request buffers, 512 B of gathered records, two barriers),
 // and the pool's in-use bitmap.
-constexpr size_t kWarpStageBytes = 2 * 32 * 16 + 32 * 16 + 16 + sizeof(NWarpState);
+// (a multiple of 16 B: the TMA destinations and uint4 records need it)
+constexpr size_t kWarpStageBytes =
+    (2 * 32 * 16 + 32 * 16 + 16 + sizeof(NWarpState) + 15) / 16 * 16;
 __host__ __device__ __forceinline__ size_t smem_cta_bytes(int buckets,
                                                           int warps) {
   return (size_t)buckets * kBucket * 16 + (size_t)warps * kWarpStageBytes +
-         (size_t)((buckets + 31) / 32) * 4 + 8;
+         (size_t)((buckets + 31) / 32) * 4 + 12;
 }
 
 // Main pass: persistent warps pull traces (longest first) from a global
@@ -988,7 +1000,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
   unsigned* used = reinterpret_cast<unsigned*>(smem + E * 16 +
                                                (size_t)WARPS * kWarpStageBytes);
   const int words = (buckets + 31) / 32;
-  for (int i = threadIdx.x; i < words + 2; i += blockDim.x) used[i] = 0u;
+  for (int i = threadIdx.x; i < words + 3; i += blockDim.x) used[i] = 0u;
   int* active = reinterpret_cast<int*>(used + words) + 1;
   if (lane == 0) {
     mbar_init(sg.bar);
@@ -1019,6 +1031,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
                  sg, lane, wire, expand);
     __syncwarp();
     if (lane == 0) atomicSub(active, 1);
+    if (results[tr].status == PM_POOL_OVERFLOW) dir.release_victim_token();
     if (lane == 0 && results[tr].status == PM_POOL_OVERFLOW) {
       const unsigned k = atomicAdd(&ctl->n_list[1], 1u);
       overflow_list[k] = tr;
