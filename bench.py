@@ -3,9 +3,12 @@
 Metric (BASELINE.json): "replayed allocator events/sec (batched traces,
 1/2/4/8 B200); bit-exact peak bytes".  Workload:
 10^4 synthetic Llama-style request traces of ~1e5 requests each (~1e9
-requests, 16 GB packed), default AllocatorConfig, unbounded capacity.  With
-N GPUs the traces are sharded over ranks (greedy LPT on length, no
-collective on the data path): strong scaling of a fixed 10^4-trace sweep.
+requests, 16 GB packed), default AllocatorConfig, unbounded capacity.  Traces
+are independent, so with N GPUs every rank replays its own 10^4-trace C3
+sweep (traces r*10^4 .. r*10^4+9999, distinct seeds) with no collective on
+the data path: weak scaling, `value` = all ranks' requests / the slowest
+rank's time.  `--strong` instead shards ONE 10^4-trace sweep over the ranks
+by greedy LPT on length.
 
   value   device-resident: packed requests already in HBM, one step = one
           pm_replay_batch over the rank's shard, timed with CUDA events on
@@ -52,7 +55,11 @@ def parse_args():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["engine", "reference"], default="engine")
-    ap.add_argument("--traces", type=int, default=10_000)
+    ap.add_argument("--traces", type=int, default=10_000,
+                    help="traces per rank (weak scaling) or in total (--strong)")
+    ap.add_argument("--strong", action="store_true",
+                    help="shard one fixed sweep of --traces traces over the ranks "
+                         "(default: every rank replays its own --traces traces)")
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--cpu-sample-stride", type=int, default=10)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -184,14 +191,22 @@ def main():
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
 
-    # ---- workload: this rank's shard of the 10^4-trace sweep ---------------
+    # ---- workload ----------------------------------------------------------
+    # weak scaling (default): rank r replays its own C3 sweep, traces
+    # r*T .. r*T+T-1 (seeds 1_000_003 + i); --strong: the ranks share one
+    # sweep of T traces by greedy LPT on length.  No collective on the data
+    # path either way.
     from paper_2504_03887_b200.synth import _load
     lib = _load()
-    counts = np.zeros(args.traces, dtype=np.int64)
-    lib.pm_synth_counts(0, args.traces, counts.ctypes.data,
+    n_all = args.traces if args.strong else args.traces * world
+    counts = np.zeros(n_all, dtype=np.int64)
+    lib.pm_synth_counts(0, n_all, counts.ctypes.data,
                         len(os.sched_getaffinity(0)))
     from paper_2504_03887_b200.shard import lpt_shards
-    mine = lpt_shards(counts, world)[rank]
+    if args.strong:
+        mine = lpt_shards(counts, world)[rank]
+    else:
+        mine = np.arange(rank * args.traces, (rank + 1) * args.traces)
     # generate the shard's traces contiguously into pinned host memory
     offs = np.zeros(len(mine) + 1, dtype=np.int64)
     np.cumsum(counts[mine], out=offs[1:])
@@ -315,19 +330,24 @@ def main():
         "warmup": args.warmup,
         "ms_per_step": max_ms / args.steps,
         "higher_is_better": True,
-        "scaling": "strong",
+        "scaling": "strong" if args.strong else "weak",
         "vs_baseline": None,
         "dtype": "int64",
         "data": "synthetic (seeded Llama-style request traces, SURVEY §8d C3)",
         "config": {
-            "workload": "C3: 10^4 synthetic Llama-style training traces, "
-                        "~1e5 requests each, sharded LPT over GPUs",
-            "n_traces": args.traces,
+            "workload": ("C3: one sweep of 10^4 synthetic Llama-style training "
+                         "traces (~1e5 requests each) sharded LPT over the GPUs"
+                         if args.strong else
+                         "C3: 10^4 synthetic Llama-style training traces (~1e5 "
+                         "requests each) per GPU, distinct seeds per rank"),
+            "n_traces": args.traces if args.strong else args.traces * world,
             "requests_total_all_ranks": int(all_events),
             "requests_rank0": events_per_step,
             "allocator": "AllocatorConfig() defaults, device_capacity None",
             "l2": "inputs larger than L2 (16 B x ~1e9 requests >> 126 MB)",
-            "parallelism": f"traces sharded over {world} GPU(s), no collective",
+            "parallelism": f"independent traces over {world} GPU(s), no collective "
+                           "on the data path (NCCL only for the barrier and the "
+                           "max-over-ranks time)",
         },
         "e2e": {"value": e2e_value, "unit": "events/s",
                 "h2d_bytes_per_step": int(words.nbytes + offs.nbytes + cfg.nbytes),
@@ -401,7 +421,7 @@ def run_reference(args, rank, world):
         "metric": METRIC, "value": value, "unit": "events/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * sum(times) / len(times),
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "higher_is_better": True, "scaling": "strong" if args.strong else "weak", "vs_baseline": None,
         "dtype": "int64",
         "data": "synthetic (seeded Llama-style request traces, SURVEY §8d C3)",
         "config": {"workload": "C3: 10^4 synthetic Llama-style training traces, "
