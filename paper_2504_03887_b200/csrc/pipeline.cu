@@ -25,6 +25,8 @@
 
 #include <cub/cub.cuh>
 #include <algorithm>
+#include <cstdint>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -823,12 +825,30 @@ int perr(int code, const std::string& m) {
   return code;
 }
 
+// The default release threshold (0) hands the stream-ordered pool's memory
+// back to the driver at every synchronisation, so each call would map its
+// scratch (GBs at C5 scale) afresh; keep it mapped between calls.
+void keep_pool_mapped() {
+  static std::mutex mu;
+  static int tuned_dev = -1;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return;
+  std::lock_guard<std::mutex> g(mu);
+  if (tuned_dev == dev) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  tuned_dev = dev;
+}
+
 // stream-ordered scratch arena, freed on destruction
 struct Arena {
   cudaStream_t s;
   std::vector<void*> ptrs;
   cudaError_t err = cudaSuccess;
-  explicit Arena(cudaStream_t st) : s(st) {}
+  explicit Arena(cudaStream_t st) : s(st) { keep_pool_mapped(); }
   template <class T>
   T* alloc(size_t n) {
     void* p = nullptr;
