@@ -76,7 +76,9 @@ typedef enum {
   PM_BAD_HANDLE = 8,       /* handle outside [0, n_events): caller bug      */
   PM_SIZE_LIMIT = 9,       /* a block >= 2^46 B: outside the engine's range */
   PM_BAD_STREAM = 10,      /* stream id >= 65536                            */
-  PM_POOL_OVERFLOW = 11    /* internal; resolved by the global-pool retry   */
+  PM_POOL_OVERFLOW = 11,   /* internal; resolved by the global-pool retry   */
+  PM_ENCODING_LIMIT = 12   /* internal; the narrow pass hands the trace to
+                              the wide (64-bit) tiers                       */
 } pm_status_t;
 
 typedef struct {

@@ -38,7 +38,7 @@ KIND_ALLOC, KIND_FREE, KIND_UNKNOWN, KIND_MISSING = 0, 1, 2, 3
 
 (PM_OK, PM_OOM, PM_UNKNOWN_HANDLE, PM_DOUBLE_FREE, PM_DUPLICATE_HANDLE,
  PM_ZERO_SIZE, PM_UNKNOWN_KIND, PM_MISSING_FIELD, PM_BAD_HANDLE,
- PM_SIZE_LIMIT, PM_BAD_STREAM, PM_POOL_OVERFLOW) = range(12)
+ PM_SIZE_LIMIT, PM_BAD_STREAM, PM_POOL_OVERFLOW, PM_ENCODING_LIMIT) = range(13)
 
 #: every symbol include/peakmem_b200.h declares
 EXPORTED_SYMBOLS = ("pm_last_error", "pm_version", "pm_replay_workspace_bytes",

@@ -52,7 +52,7 @@ Layout layout_for(int64_t total_events, int64_t max_trace_events,
   Layout L;
   size_t off = align_up(sizeof(pmb::Ctl), 256);
   L.retry_list = off;
-  off = align_up(off + 4 * sizeof(int32_t) * (size_t)(n_traces > 0 ? n_traces : 1),
+  off = align_up(off + 6 * sizeof(int32_t) * (size_t)(n_traces > 0 ? n_traces : 1),
                  256);
   const int64_t mx = max_trace_events > 0 ? max_trace_events : 1;
   L.nbmax_g = (int)(mx / 8 + 4);
@@ -71,6 +71,10 @@ struct Occupancy {
   int sms = 0, per_sm = 0, buckets = 0, warps = 0;
   size_t smem = 0;
   bool narrow = true;  // main pass: replay_narrow_kernel (else the wide kernel)
+  int per_sm_n = 0, buckets_n = 0;  // the narrow main kernel's launch
+  size_t smem_n = 0;
+  int nbmax_m1 = 0, nbmax_m2 = 0;   // narrow memory-directory passes 1-2
+  size_t smem_m1 = 0;
   int per_sm1 = 0;  // tier-1 retry kernel
   size_t smem1 = 0;
   int nbmax2 = 0;   // tier-2: one warp with a shared-memory directory
@@ -144,21 +148,24 @@ int query_occupancy(Occupancy* out) {
     o.warps = o.narrow ? kNarrowWarps : kWarps;
     if (const char* env = getenv("PM_REPLAY_WARPS")) o.warps = atoi(env);
     int rc;
+    // the narrow main kernel is always set up (wire-word input needs it even
+    // when PM_REPLAY_WIDE selects the wide main pass)
+    const int nw = o.narrow ? o.warps : kNarrowWarps;
+    switch (nw) {
+      case 12: rc = setup_narrow<12>(optin, cap, &o.buckets_n, &o.smem_n, &o.per_sm_n); break;
+      case 20: rc = setup_narrow<20>(optin, cap, &o.buckets_n, &o.smem_n, &o.per_sm_n); break;
+      case 24: rc = setup_narrow<24>(optin, cap, &o.buckets_n, &o.smem_n, &o.per_sm_n); break;
+      case 28: rc = setup_narrow<28>(optin, cap, &o.buckets_n, &o.smem_n, &o.per_sm_n); break;
+      case 32: rc = setup_narrow<32>(optin, cap, &o.buckets_n, &o.smem_n, &o.per_sm_n); break;
+      default:
+        if (o.narrow) o.warps = 16;
+        rc = setup_narrow<16>(optin, cap, &o.buckets_n, &o.smem_n, &o.per_sm_n);
+    }
+    if (rc != PM_SUCCESS) return rc;
     if (o.narrow) {
-      if (o.warps == 12)
-        rc = setup_narrow<12>(optin, cap, &o.buckets, &o.smem, &o.per_sm);
-      else if (o.warps == 20)
-        rc = setup_narrow<20>(optin, cap, &o.buckets, &o.smem, &o.per_sm);
-      else if (o.warps == 24)
-        rc = setup_narrow<24>(optin, cap, &o.buckets, &o.smem, &o.per_sm);
-      else if (o.warps == 28)
-        rc = setup_narrow<28>(optin, cap, &o.buckets, &o.smem, &o.per_sm);
-      else if (o.warps == 32)
-        rc = setup_narrow<32>(optin, cap, &o.buckets, &o.smem, &o.per_sm);
-      else {
-        o.warps = 16;
-        rc = setup_narrow<16>(optin, cap, &o.buckets, &o.smem, &o.per_sm);
-      }
+      o.buckets = o.buckets_n;
+      o.smem = o.smem_n;
+      o.per_sm = o.per_sm_n;
     } else if (o.warps == 12)
       rc = setup_kernel<12>(optin, cap, &o.buckets, &o.smem, &o.per_sm);
     else if (o.warps == 14)
@@ -167,6 +174,20 @@ int query_occupancy(Occupancy* out) {
       o.warps = 16;
       rc = setup_kernel<16>(optin, cap, &o.buckets, &o.smem, &o.per_sm);
     }
+    if (rc != PM_SUCCESS) return rc;
+    // narrow memory-directory passes: one warp per CTA, 24 B of directory
+    // per bucket, + 512 B of entries per bucket in the shared-memory pass
+    o.nbmax_m1 = (int)(((size_t)optin - pmn::kWarpStageBytes - 256) / (24 + 512));
+    o.smem_m1 = pmn::mem_tier_smem(o.nbmax_m1, true);
+    o.nbmax_m2 = (int)(((size_t)optin - pmn::kWarpStageBytes - 256) / 24);
+    e = cudaFuncSetAttribute(pmn::replay_narrow_mem_kernel<true>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)o.smem_m1);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute pass 1");
+    e = cudaFuncSetAttribute(pmn::replay_narrow_mem_kernel<false>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)pmn::mem_tier_smem(o.nbmax_m2, false));
+    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute pass 2");
     if (rc != PM_SUCCESS) return rc;
     int b1 = 0;
     rc = setup_kernel<kTier1Warps>(optin, kTier1Warps * 32, &b1, &o.smem1,
@@ -194,6 +215,8 @@ int query_occupancy(Occupancy* out) {
           (const void*)pmn::replay_narrow_kernel<12>, (const void*)pmn::replay_narrow_kernel<16>,
           (const void*)pmn::replay_narrow_kernel<20>, (const void*)pmn::replay_narrow_kernel<24>,
           (const void*)pmn::replay_narrow_kernel<28>, (const void*)pmn::replay_narrow_kernel<32>,
+          (const void*)pmn::replay_narrow_mem_kernel<true>,
+          (const void*)pmn::replay_narrow_mem_kernel<false>,
           (const void*)pmb::replay_smem_kernel<8>, (const void*)pmb::replay_smem_kernel<12>,
           (const void*)pmb::replay_smem_kernel<14>, (const void*)pmb::replay_smem_kernel<16>,
           (const void*)pmb::replay_dirmem_kernel<1, 0>,
@@ -305,38 +328,44 @@ int replay_batch_impl(const pm_req_t* reqs, const int64_t* trace_offsets,
 
   cudaError_t e = cudaMemsetAsync(ctl, 0, sizeof(pmb::Ctl), stream);
   if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync");
-  int32_t* list1 = retry_list;
-  int32_t* list2 = retry_list + n_traces;
-  long long want = ((long long)n_traces + occ.warps - 1) / occ.warps;
-  long long grid = (long long)occ.per_sm * occ.sms;
+  // pass lists (pmn::route): narrow memory-directory tiers, then the wide
+  // tiers 1-4 (an encoding limit goes straight to wide tier 1)
+  const size_t nt = (size_t)n_traces;
+  int32_t* list_m1 = retry_list;           // pass 1: narrow, smem entries
+  int32_t* list_m2 = retry_list + nt;      // pass 2: narrow, HBM entries
+  int32_t* list_w1 = retry_list + 2 * nt;  // pass 3: wide tier 1
+  int32_t* list_w2 = retry_list + 3 * nt;  // pass 4: wide tier 2
+  int32_t* list_w3 = retry_list + 4 * nt;  // pass 5: wide tier 3
+  int32_t* list_w4 = retry_list + 5 * nt;  // pass 6: wide tier 4
+  const bool narrow = occ.narrow || wire != nullptr;  // wire words need it
+  const int mwarps = narrow && !occ.narrow ? kNarrowWarps : occ.warps;
+  long long want = ((long long)n_traces + mwarps - 1) / mwarps;
+  long long grid = (long long)(narrow && !occ.narrow ? occ.per_sm_n : occ.per_sm) * occ.sms;
   if (want < grid) grid = want;
   if (const char* cap = getenv("PM_MAX_GRID")) {  // debugging aid
     const long long g = atoll(cap);
     if (g > 0 && g < grid) grid = g;
   }
 #define PM_LAUNCH_NARROW(W)                                                   \
-  pmn::replay_narrow_kernel<W><<<(unsigned)grid, W * 32, occ.smem, stream>>>( \
+  pmn::replay_narrow_kernel<W><<<(unsigned)grid, W * 32, occ.smem_n, stream>>>( \
       reqs, trace_offsets, cfgs, cfg_of_trace, results, timeline,             \
-      reinterpret_cast<pmb::u32*>(recs), ctl, trace_order, n_traces, list1,   \
-      occ.buckets, group_end, n_groups, ready,                               \
-      reinterpret_cast<const pmb::u64*>(wire), const_cast<pm_req_t*>(reqs))
+      reinterpret_cast<pmb::u32*>(recs), ctl, trace_order, n_traces, list_m1, \
+      occ.buckets_n, group_end, n_groups, ready,                             \
+      reinterpret_cast<const pmb::u64*>(wire), const_cast<pm_req_t*>(reqs),   \
+      list_w1)
 #define PM_LAUNCH_MAIN(W)                                                     \
   pmb::replay_smem_kernel<W><<<(unsigned)grid, W * 32, occ.smem, stream>>>(  \
       reqs, trace_offsets, cfgs, cfg_of_trace, results, timeline, recs, ctl, \
-      0, trace_order, n_traces, list1, occ.buckets, group_end, n_groups, ready)
-  if (occ.narrow) {
-    if (occ.warps == 12)
-      PM_LAUNCH_NARROW(12);
-    else if (occ.warps == 20)
-      PM_LAUNCH_NARROW(20);
-    else if (occ.warps == 24)
-      PM_LAUNCH_NARROW(24);
-    else if (occ.warps == 28)
-      PM_LAUNCH_NARROW(28);
-    else if (occ.warps == 32)
-      PM_LAUNCH_NARROW(32);
-    else
-      PM_LAUNCH_NARROW(16);
+      0, trace_order, n_traces, list_m1, occ.buckets, group_end, n_groups, ready)
+  if (narrow) {
+    switch (mwarps) {
+      case 12: PM_LAUNCH_NARROW(12); break;
+      case 20: PM_LAUNCH_NARROW(20); break;
+      case 24: PM_LAUNCH_NARROW(24); break;
+      case 28: PM_LAUNCH_NARROW(28); break;
+      case 32: PM_LAUNCH_NARROW(32); break;
+      default: PM_LAUNCH_NARROW(16); break;
+    }
   } else if (occ.warps == 12)
     PM_LAUNCH_MAIN(12);
   else if (occ.warps == 14)
@@ -346,48 +375,67 @@ int replay_batch_impl(const pm_req_t* reqs, const int64_t* trace_offsets,
 #undef PM_LAUNCH_MAIN
 #undef PM_LAUNCH_NARROW
   e = cudaGetLastError();
-  if (e != cudaSuccess) return cuda_fail(e, "replay_smem_kernel launch");
+  if (e != cudaSuccess) return cuda_fail(e, "replay main-pass launch");
   if (after_main) {
     // streamed input: the copies go in behind the main pass (which waits
     // on their flags) and before any further launch
     const int rc2 = after_main();
     if (rc2 != PM_SUCCESS) return rc2;
   }
-  // tier 1: dedicated 32-bucket pools (grid sized for the worst case; idle
-  // CTAs exit at once when nothing overflowed)
+  const long long gtraces = n_traces < occ.sms ? n_traces : occ.sms;
+  // passes 1-2: narrow, shared-memory directory (entries in shared memory,
+  // then in HBM: the per-CTA region fits in tier 4's, nb <= nbmax_g)
+  pmn::replay_narrow_mem_kernel<true><<<(unsigned)gtraces, 32, occ.smem_m1, stream>>>(
+      reqs, trace_offsets, cfgs, cfg_of_trace, results, timeline,
+      reinterpret_cast<pmb::u32*>(recs), ctl, pmn::kTierMemSmem, list_m1, list_m2,
+      list_w1, nullptr, occ.nbmax_m1, reinterpret_cast<const pmb::u64*>(wire),
+      const_cast<pm_req_t*>(reqs));
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "replay pass-1 launch");
+  {
+    const int nbm2 = occ.nbmax_m2 < L.nbmax_g ? occ.nbmax_m2 : L.nbmax_g;
+    const long long gm2 = L.retry_warps < occ.sms ? L.retry_warps : occ.sms;
+    pmn::replay_narrow_mem_kernel<false>
+        <<<(unsigned)gm2, 32, pmn::mem_tier_smem(nbm2, false), stream>>>(
+            reqs, trace_offsets, cfgs, cfg_of_trace, results, timeline,
+            reinterpret_cast<pmb::u32*>(recs), ctl, pmn::kTierMemHbm, list_m2,
+            list_w4, list_w1, gpool, nbm2, reinterpret_cast<const pmb::u64*>(wire),
+            const_cast<pm_req_t*>(reqs));
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "replay pass-2 launch");
+  }
+  // wide tier 1 (pass 3): dedicated 32-bucket pools (grid sized for the
+  // worst case; idle CTAs exit at once when nothing was escalated)
   long long grid1 = (long long)occ.per_sm1 * occ.sms;
   long long want1 = ((long long)n_traces + kTier1Warps - 1) / kTier1Warps;
   if (want1 < grid1) grid1 = want1;
   pmb::replay_smem_kernel<kTier1Warps>
       <<<(unsigned)grid1, kTier1Warps * 32, occ.smem1, stream>>>(
           reqs, trace_offsets, cfgs, cfg_of_trace, results, timeline, recs,
-          ctl, 1, list1, 0, list2, kTier1Warps * 32, nullptr, 0, nullptr);
+          ctl, pmn::kTierWide1, list_w1, 0, list_w2, kTier1Warps * 32, nullptr,
+          0, nullptr);
   e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "replay tier-1 launch");
   {
-    int32_t* list3 = retry_list + 2 * (size_t)n_traces;
-    long long grid2 = occ.sms;
-    if (n_traces < grid2) grid2 = n_traces;
-    pmb::replay_dirmem_kernel<1, 0><<<(unsigned)grid2, 32, occ.smem2, stream>>>(
+    pmb::replay_dirmem_kernel<1, 0><<<(unsigned)gtraces, 32, occ.smem2, stream>>>(
         reqs, trace_offsets, cfgs, cfg_of_trace, results, timeline, recs, ctl,
-        2, list2, list3, nullptr, occ.nbmax2);
+        pmn::kTierWide1 + 1, list_w2, list_w3, nullptr, occ.nbmax2);
     e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "replay tier-2 launch");
     // tier 3: shared-memory directory, HBM entries (the per-warp pool fits
     // in tier 4's region: nbmax3 is capped at tier 4's bucket count)
-    int32_t* list4 = retry_list + 3 * (size_t)n_traces;
     const int nb3 = occ.nbmax3 < L.nbmax_g ? occ.nbmax3 : L.nbmax_g;
     long long grid3 = L.retry_warps < occ.sms ? L.retry_warps : occ.sms;
     pmb::replay_dirmem_kernel<1, 1><<<(unsigned)grid3, 32, pmb::hybrid_smem_bytes(nb3),
                                       stream>>>(
         reqs, trace_offsets, cfgs, cfg_of_trace, results, timeline, recs, ctl,
-        3, list3, list4, gpool, nb3);
+        pmn::kTierWide1 + 2, list_w3, list_w4, gpool, nb3);
     e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "replay tier-3 launch");
     pmb::replay_dirmem_kernel<kRetryWarps, 2>
         <<<L.retry_warps / kRetryWarps, kRetryWarps * 32, 0, stream>>>(
             reqs, trace_offsets, cfgs, cfg_of_trace, results, timeline, recs,
-            ctl, 4, list4, nullptr, gpool, L.nbmax_g);
+            ctl, pmn::kTierWide4, list_w4, nullptr, gpool, L.nbmax_g);
   }
   e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "replay tier-4 launch");

@@ -26,9 +26,11 @@
 // The encoding covers one stream (stream 0) and next_base_u < 2^32 - 1
 // (2 TiB of segments ever reserved at u = 512).  A trace that leaves it
 // (another stream, a larger block or address space) stops with
-// PM_POOL_OVERFLOW and is replayed from the start by the wide tiers
-// (replay_device.cuh), exactly like a trace whose free blocks outgrow the
-// shared pool; results are bit-identical either way.
+// PM_ENCODING_LIMIT and is replayed from the start by the wide tiers
+// (replay_device.cuh); a trace whose free blocks outgrow the main pass's
+// 32-bucket register directory or the CTA pool stops with PM_POOL_OVERFLOW
+// and is replayed by the narrow memory-directory tiers below.  Results are
+// bit-identical whichever tier finishes a trace.
 #pragma once
 
 #include "replay_device.cuh"
@@ -241,6 +243,12 @@ struct NWarpState {
   int nseg, nseg_peak, maxF;  // maxF: free-block high-water mark
 };
 
+// Per-warp staging area: two 512 B request buffers (TMA destinations), 512 B
+// of gathered records, two mbarriers, the warp state -- a multiple of 16 B
+// (the TMA destinations and uint4 records need it).
+constexpr size_t kWarpStageBytes =
+    (2 * 32 * 16 + 32 * 16 + 16 + sizeof(NWarpState) + 15) / 16 * 16;
+
 // ---- record refs (global store + staged mirror) ---------------------------
 
 __device__ __forceinline__ void set_link(const NRecs& rec, uint4* st, int hcmp,
@@ -295,7 +303,8 @@ __device__ __forceinline__ int argmin_pk(bool valid, u64 x) {
 
 // Merge the first adjacent bucket pair whose entries fit in one bucket: the
 // right bucket's entries move into the left one's free slots.
-__device__ __forceinline__ bool try_merge(const NPool& P, NDir& dir,
+template <class D>
+__device__ __forceinline__ bool try_merge(const NPool& P, D& dir,
                                           const NRecs& rec, uint4* st,
                                           int hcmp, int lane) {
   const int e = dir.mergeable();
@@ -329,7 +338,8 @@ __device__ __forceinline__ bool try_merge(const NPool& P, NDir& dir,
 // Split the full bucket at position d: the upper half by ka rank moves to a
 // new bucket (slots 0..15), the lower half stays in place.  False if no
 // bucket can be had and nothing merges (overflow).
-__device__ __forceinline__ bool split_bucket(const NPool& P, NDir& dir, int d,
+template <class D>
+__device__ __forceinline__ bool split_bucket(const NPool& P, D& dir, int d,
                                              const NRecs& rec, uint4* st,
                                              int hcmp, int lane) {
   int q = dir.full() ? -1 : dir.alloc_phys();
@@ -365,7 +375,8 @@ __device__ __forceinline__ bool split_bucket(const NPool& P, NDir& dir, int d,
 }
 
 // Insert a free block; returns its id or -1 on pool overflow.
-__device__ __forceinline__ int pool_insert(const NPool& P, NDir& dir, NCtx& c,
+template <class D>
+__device__ __forceinline__ int pool_insert(const NPool& P, D& dir, NCtx& c,
                                            u64 ka, u64 links, const NRecs& rec,
                                            uint4* st, int hcmp, int lane) {
   if (dir.nb == 0) {
@@ -395,7 +406,8 @@ __device__ __forceinline__ int pool_insert(const NPool& P, NDir& dir, NCtx& c,
 
 // Remove free block `id`: clear its slot (nothing moves); an emptied bucket
 // leaves the directory unless it is the last one.
-__device__ __forceinline__ void pool_remove(NDir& dir, NCtx& c, int id) {
+template <class D>
+__device__ __forceinline__ void pool_remove(D& dir, NCtx& c, int id) {
   const int p = id / kBucket;
   const int d = dir.pos_of_phys(p);
   PM_STAT(2);
@@ -411,7 +423,8 @@ __device__ __forceinline__ void pool_remove(NDir& dir, NCtx& c, int id) {
 // Rekey entry `id` to (ka, links) -- in place when it stays in its bucket
 // -- or, with id < 0, insert a new entry.  Returns the entry's id (-1 on
 // overflow); the caller re-points the neighbours whose refs changed.
-__device__ __forceinline__ int pool_upsert(const NPool& P, NDir& dir, NCtx& c,
+template <class D>
+__device__ __forceinline__ int pool_upsert(const NPool& P, D& dir, NCtx& c,
                                            int id, u64 ka, u64 links,
                                            const NRecs& rec, uint4* st,
                                            int hcmp, int lane) {
@@ -435,7 +448,8 @@ __device__ __forceinline__ int pool_upsert(const NPool& P, NDir& dir, NCtx& c,
 // size_u - ru <= kMaxU - 1 always).  The bucket holding ru and the next
 // one are loaded together; the next one's minimum is the only candidate
 // when the first holds none.
-__device__ __forceinline__ int best_fit(const NPool& P, const NDir& dir,
+template <class D>
+__device__ __forceinline__ int best_fit(const NPool& P, const D& dir,
                                         u32 ru, u32 span, int lane) {
   if (dir.nb == 0) return -1;
   const int d = dir.find((u64)ru << 32);
@@ -461,8 +475,9 @@ __device__ __forceinline__ int best_fit(const NPool& P, const NDir& dir,
 
 // Wholly-free segment (entry with no allocated neighbour) of largest size_u
 // > thr (thr < 0: any), ties lowest addr; -1 if none.
+template <class D>
 __device__ __forceinline__ int find_release_candidate(const NPool& P,
-                                                      const NDir& dir,
+                                                      const D& dir,
                                                       long long thr, int lane) {
   u64 best = ~0ull;
   int bid = -1;
@@ -484,7 +499,8 @@ __device__ __forceinline__ int find_release_candidate(const NPool& P,
   return w < 0 ? -1 : __shfl_sync(kFull, bid, w);
 }
 
-__device__ __forceinline__ void make_room(const NPool& P, NDir& dir, NCtx& c,
+template <class D>
+__device__ __forceinline__ void make_room(const NPool& P, D& dir, NCtx& c,
                                           long long seg, NWarpState* ws, int s,
                                           const NRecs& rec, uint4* st,
                                           int hcmp, int lane) {
@@ -569,12 +585,14 @@ __device__ __forceinline__ int ctz64(long long v) {
 
 // ---- one trace ---------------------------------------------------------------
 
+template <class D>
 __device__ __forceinline__ void replay_trace(
     int tr, const pm_req_t* __restrict__ reqs, const int64_t* __restrict__ offs,
     const pm_cfg_t* __restrict__ cfgs, const int32_t* __restrict__ cfg_of,
     pm_result_t* __restrict__ results, int64_t* __restrict__ timeline,
-    u32* rec_base, const NPool& P, NDir& dir, NStage& sg, int lane,
-    const u64* __restrict__ wire, pm_req_t* __restrict__ expand) {
+    u32* rec_base, const NPool& P, D& dir, NStage& sg, int lane,
+    const u64* __restrict__ wire, pm_req_t* __restrict__ expand,
+    bool expand_overflow) {
   const long long e0 = offs[tr];
   const int n = (int)(offs[tr + 1] - e0);  // < 2^31 (pm_replay_batch)
   const pm_cfg_t* cp = cfgs + (cfg_of ? cfg_of[tr] : 0);
@@ -732,7 +750,7 @@ __device__ __forceinline__ void replay_trace(
           } else if ((ks >> 2) != 0u ||
                      ((((u64)size + ws->amask) & ~(u64)ws->amask) >> s) >
                          (u64)ws->lim) {
-            sts = PM_POOL_OVERFLOW;  // outside the encoding: wide tiers
+            sts = PM_ENCODING_LIMIT;  // outside the encoding: wide tiers
           } else {
             const u32 ru = (u32)((((u64)size + ws->amask) & ~(u64)ws->amask) >> s);
             const u32 split_lim = ws->split_lim;
@@ -773,7 +791,7 @@ __device__ __forceinline__ void replay_trace(
               const u64 seg_u = (u64)seg >> s;
               const u32 A = ws->next_base;
               if (sts == PM_OK && (u64)A + seg_u > kMaxU)
-                sts = PM_POOL_OVERFLOW;
+                sts = PM_ENCODING_LIMIT;
               if (sts == PM_OK) {
                 c.reserved += seg;
                 {
@@ -908,7 +926,9 @@ __device__ __forceinline__ void replay_trace(
     }
   }
 
-  if (wire != nullptr && status == PM_POOL_OVERFLOW) {
+  if (wire != nullptr &&
+      (status == PM_ENCODING_LIMIT ||
+       (status == PM_POOL_OVERFLOW && expand_overflow))) {
     // the wide tiers read pm_req_t: expand this trace's words for them
     int ab = 0;
     for (int i0 = 0; i0 < n; i0 += 32) {
@@ -955,12 +975,184 @@ __device__ __forceinline__ void replay_trace(
   }
 }
 
+__device__ __forceinline__ NStage carve_stage(char* wst) {
+  NStage sg;
+  sg.buf = reinterpret_cast<ulonglong2*>(wst);
+  sg.rec = reinterpret_cast<uint4*>(wst + 2 * 32 * 16);
+  sg.bar = reinterpret_cast<u64*>(wst + 3 * 32 * 16);
+  sg.ws = reinterpret_cast<NWarpState*>(wst + 3 * 32 * 16 + 16);
+  sg.g = 0;
+  return sg;
+}
+
+// ---- escalation routing ------------------------------------------------------
+//
+// Passes of one pm_replay_batch, in launch order (Ctl work / n_list index):
+//   0 main narrow pass (register directory, CTA-shared pool)
+//   1 narrow, memory directory, entries in shared memory   (kTierMemSmem)
+//   2 narrow, memory directory, entries in HBM              (kTierMemHbm)
+//   3..6 the wide tiers 1-4 of replay_device.cuh            (kTierWide1..)
+// A capacity overflow moves a trace to the next capacity tier; an encoding
+// limit sends it to the first wide tier.
+constexpr int kTierMemSmem = 1;
+constexpr int kTierMemHbm = 2;
+constexpr int kTierWide1 = 3;
+constexpr int kTierWide4 = 6;
+
+__device__ __forceinline__ void route(pmb::Ctl* ctl, int sts, int tr,
+                                      int next_pass,
+                                      int32_t* __restrict__ overflow_list,
+                                      int32_t* __restrict__ enc_list) {
+  if (sts == PM_POOL_OVERFLOW) {
+    overflow_list[atomicAdd(&ctl->n_list[next_pass], 1u)] = tr;
+  } else if (sts == PM_ENCODING_LIMIT) {
+    enc_list[atomicAdd(&ctl->n_list[kTierWide1], 1u)] = tr;
+  }
+}
+
+// Directory in shared memory (one warp per CTA, any number of buckets up
+// to nbmax): bounds and physical ids by position, occupancy masks and
+// positions by physical bucket, a stack of free physical buckets.  Same
+// interface as NDir; find is a 32-ary warp search over the sorted bounds.
+struct NDirMem {
+  u64* db;          // [nbmax] bound by position
+  int* dp;          // [nbmax] physical bucket by position
+  unsigned* m;      // [nbmax] occupancy mask by physical bucket
+  int* pos;         // [nbmax] position by physical bucket
+  int* pstack;      // [nbmax] free physical buckets
+  int nb, ptop, nbmax, lane;
+
+  __device__ __forceinline__ void init(int lane_) {
+    lane = lane_;
+    nb = 0;
+    __syncwarp();
+    for (int i = lane; i < nbmax; i += 32) pstack[i] = nbmax - 1 - i;
+    __syncwarp();
+    ptop = nbmax;
+  }
+  // last position whose bound <= x: each round probes 32 evenly spaced
+  // positions of the live range, shrinking it 32x
+  __device__ __forceinline__ int find(u64 x) const {
+    int lo_ = 0, hi_ = nb;
+    while (hi_ - lo_ > 32) {
+      const int step = (hi_ - lo_ + 31) / 32;
+      const int e = lo_ + lane * step;
+      const unsigned b = __ballot_sync(kFull, e < hi_ && db[e] <= x);
+      lo_ += (31 - __clz(b)) * step;  // lane 0 probes lo_: always true
+      hi_ = min(lo_ + step, hi_);
+    }
+    const int e = lo_ + lane;
+    const unsigned b = __ballot_sync(kFull, e < hi_ && db[e] <= x);
+    return b ? lo_ + 31 - __clz(b) : lo_;
+  }
+  __device__ __forceinline__ int phys(int d) const { return dp[d]; }
+  __device__ __forceinline__ unsigned mask(int d) const { return m[dp[d]]; }
+  __device__ __forceinline__ void set_mask(int d, unsigned v) {
+    const int p = dp[d];
+    __syncwarp();
+    m[p] = v;  // uniform store
+    __syncwarp();
+  }
+  __device__ __forceinline__ void set_bit(int d, int b) {
+    set_mask(d, mask(d) | (1u << b));
+  }
+  __device__ __forceinline__ void clear_bit(int d, int b) {
+    set_mask(d, mask(d) & ~(1u << b));
+  }
+  __device__ __forceinline__ int pos_of_phys(int p) const { return pos[p]; }
+  __device__ __forceinline__ int mergeable() const {
+    for (int base = 0; base < nb - 1; base += 32) {
+      const int x = base + lane;
+      bool ok = false;
+      if (x < nb - 1) ok = __popc(m[dp[x]]) + __popc(m[dp[x + 1]]) <= kBucket;
+      const unsigned b = __ballot_sync(kFull, ok);
+      if (b) return base + __ffs(b) - 1;
+    }
+    return -1;
+  }
+  __device__ __forceinline__ void insert(int d, u64 b, int p, unsigned mk) {
+    // shift positions d.. up by one, 32 at a time from the top
+    for (int base = ((nb - 1 - d) / 32) * 32; base >= 0; base -= 32) {
+      const int e = d + base + lane;
+      const bool mv = e < nb;
+      u64 xb = 0;
+      int xp = 0;
+      if (mv) {
+        xb = db[e];
+        xp = dp[e];
+      }
+      __syncwarp();
+      if (mv) {
+        db[e + 1] = xb;
+        dp[e + 1] = xp;
+        pos[xp] = e + 1;
+      }
+      __syncwarp();
+    }
+    db[d] = b;
+    dp[d] = p;
+    m[p] = mk;
+    pos[p] = d;
+    __syncwarp();
+    nb += 1;
+  }
+  __device__ __forceinline__ void erase(int d) {
+    for (int base = 0; d + 1 + base < nb; base += 32) {
+      const int e = d + 1 + base + lane;
+      const bool mv = e < nb;
+      u64 xb = 0;
+      int xp = 0;
+      if (mv) {
+        xb = db[e];
+        xp = dp[e];
+      }
+      __syncwarp();
+      if (mv) {
+        db[e - 1] = xb;
+        dp[e - 1] = xp;
+        pos[xp] = e - 1;
+      }
+      __syncwarp();
+    }
+    nb -= 1;
+    if (d == 0) db[0] = 0;  // uniform store
+    __syncwarp();
+  }
+  __device__ __forceinline__ int alloc_phys() {
+    if (ptop == 0) return -1;
+    ptop -= 1;
+    return pstack[ptop];
+  }
+  __device__ __forceinline__ int alloc_phys_wait() { return alloc_phys(); }
+  __device__ __forceinline__ void free_phys(int p) {
+    __syncwarp();
+    pstack[ptop] = p;  // uniform store
+    __syncwarp();
+    ptop += 1;
+  }
+  __device__ __forceinline__ void release_all() { nb = 0; }
+  __device__ __forceinline__ void release_victim_token() {}
+  __device__ __forceinline__ bool full() const { return nb >= nbmax; }
+};
+
+// Shared memory of a memory-directory tier CTA (one warp): staging, the
+// directory arrays (24 B per bucket) and, when SMEM_POOL, the entries
+// (512 B per bucket).
+__host__ __device__ __forceinline__ size_t mem_dir_bytes(int nbmax) {
+  return (size_t)nbmax * 24;
+}
+__host__ __device__ __forceinline__ size_t mem_tier_smem(int nbmax, bool smem_pool) {
+  return kWarpStageBytes + mem_dir_bytes(nbmax) +
+         (smem_pool ? (size_t)nbmax * kBucket * 16 : 0);
+}
+__host__ __device__ __forceinline__ size_t mem_tier_pool_bytes(int nbmax) {
+  return ((size_t)nbmax * kBucket * 16 + 255) / 256 * 256;
+}
+
 // Shared memory per CTA: the pool (B x 32 x 16 B), per warp a staging area
 // (two 512 B request buffers, 512 B of gathered records, two barriers),
 // and the pool's in-use bitmap.
-// (a multiple of 16 B: the TMA destinations and uint4 records need it)
-constexpr size_t kWarpStageBytes =
-    (2 * 32 * 16 + 32 * 16 + 16 + sizeof(NWarpState) + 15) / 16 * 16;
+
 __host__ __device__ __forceinline__ size_t smem_cta_bytes(int buckets,
                                                           int warps) {
   return (size_t)buckets * kBucket * 16 + (size_t)warps * kWarpStageBytes +
@@ -982,7 +1174,8 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
                          int buckets, const unsigned* __restrict__ group_end,
                          int n_groups, const volatile unsigned* ready,
                          const u64* __restrict__ wire,
-                         pm_req_t* __restrict__ expand) {
+                         pm_req_t* __restrict__ expand,
+                         int32_t* __restrict__ enc_list) {
   extern __shared__ __align__(16) char smem[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
@@ -990,13 +1183,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
   NPool P;
   P.ka = reinterpret_cast<u64*>(smem);
   P.ln = P.ka + E;
-  char* wst = smem + E * 16 + (size_t)wib * kWarpStageBytes;
-  NStage sg;
-  sg.buf = reinterpret_cast<ulonglong2*>(wst);
-  sg.rec = reinterpret_cast<uint4*>(wst + 2 * 32 * 16);
-  sg.bar = reinterpret_cast<u64*>(wst + 3 * 32 * 16);
-  sg.ws = reinterpret_cast<NWarpState*>(wst + 3 * 32 * 16 + 16);
-  sg.g = 0;
+  NStage sg = carve_stage(smem + E * 16 + (size_t)wib * kWarpStageBytes);
   unsigned* used = reinterpret_cast<unsigned*>(smem + E * 16 +
                                                (size_t)WARPS * kWarpStageBytes);
   const int words = (buckets + 31) / 32;
@@ -1028,14 +1215,70 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
     const int tr = list ? list[t] : (int)t;
     if (lane == 0) atomicAdd(active, 1);
     replay_trace(tr, reqs, offs, cfgs, cfg_of, results, timeline, recs, P, dir,
-                 sg, lane, wire, expand);
+                 sg, lane, wire, expand, false);
     __syncwarp();
     if (lane == 0) atomicSub(active, 1);
-    if (results[tr].status == PM_POOL_OVERFLOW) dir.release_victim_token();
-    if (lane == 0 && results[tr].status == PM_POOL_OVERFLOW) {
-      const unsigned k = atomicAdd(&ctl->n_list[1], 1u);
-      overflow_list[k] = tr;
-    }
+    const int sts = results[tr].status;
+    if (sts == PM_POOL_OVERFLOW) dir.release_victim_token();
+    if (lane == 0) route(ctl, sts, tr, kTierMemSmem, overflow_list, enc_list);
+  }
+}
+
+// Memory-directory tiers (passes 1 and 2): one warp per CTA replays the
+// traces whose free blocks outgrew the main pass's register directory or
+// CTA pool, with the directory in shared memory and the entries in shared
+// memory (SMEM_POOL) or in a per-CTA HBM region.
+template <bool SMEM_POOL>
+__global__ void __launch_bounds__(32, 1)
+    replay_narrow_mem_kernel(const pm_req_t* __restrict__ reqs,
+                             const int64_t* __restrict__ offs,
+                             const pm_cfg_t* __restrict__ cfgs,
+                             const int32_t* __restrict__ cfg_of,
+                             pm_result_t* __restrict__ results,
+                             int64_t* __restrict__ timeline, u32* recs,
+                             pmb::Ctl* ctl, int pass,
+                             const int32_t* __restrict__ list,
+                             int32_t* __restrict__ overflow_list,
+                             int32_t* __restrict__ enc_list,
+                             char* __restrict__ gpool, int nbmax,
+                             const u64* __restrict__ wire,
+                             pm_req_t* __restrict__ expand) {
+  extern __shared__ __align__(16) char smem[];
+  const int lane = threadIdx.x & 31;
+  NStage sg = carve_stage(smem);
+  char* dbase = smem + kWarpStageBytes;
+  NDirMem dir;
+  dir.nbmax = nbmax;
+  dir.db = reinterpret_cast<u64*>(dbase);
+  dir.dp = reinterpret_cast<int*>(dir.db + nbmax);
+  dir.m = reinterpret_cast<unsigned*>(dir.dp + nbmax);
+  dir.pos = reinterpret_cast<int*>(dir.m + nbmax);
+  dir.pstack = dir.pos + nbmax;
+  NPool P;
+  char* pbase = SMEM_POOL ? dbase + mem_dir_bytes(nbmax)
+                          : gpool + (size_t)blockIdx.x * mem_tier_pool_bytes(nbmax);
+  P.ka = reinterpret_cast<u64*>(pbase);
+  P.ln = P.ka + (size_t)nbmax * kBucket;
+  if (lane == 0) {
+    mbar_init(sg.bar);
+    mbar_init(sg.bar + 1);
+    mbar_fence_init();
+  }
+  __syncwarp();
+  const unsigned n = ctl->n_list[pass];
+  for (;;) {
+    unsigned t = 0;
+    if (lane == 0) t = atomicAdd(&ctl->work[pass], 1u);
+    t = __shfl_sync(kFull, t, 0);
+    if (t >= n) break;
+    const int tr = list[t];
+    // the last narrow tier expands wire words for the wide tier it hands to
+    replay_trace(tr, reqs, offs, cfgs, cfg_of, results, timeline, recs, P, dir,
+                 sg, lane, wire, expand, !SMEM_POOL);
+    __syncwarp();
+    if (lane == 0)
+      route(ctl, results[tr].status, tr, SMEM_POOL ? kTierMemHbm : kTierWide4,
+            overflow_list, enc_list);
   }
 }
 

@@ -352,20 +352,22 @@ def _holes(n_holes, fill):
     return seq
 
 
-def test_retry_tiers_3_and_4_vs_oracle():
-    # 20k holes stay in tier 3; 240k holes outgrow its ~7k-bucket shared
-    # directory and finish in tier 4 (everything in HBM)
-    traces = [_holes(20_000, 2_000), _holes(240_000, 3_000)]
+def test_retry_passes_vs_oracle():
+    # 2k holes outgrow the main pass's 32-bucket register directory and
+    # finish in pass 1 (shared-memory directory and entries); 20k outgrow
+    # its ~430 buckets and finish in pass 2 (HBM entries); 400k outgrow pass
+    # 2's ~9.6k-bucket directory and finish in wide tier 4
+    traces = [_holes(2_000, 500), _holes(20_000, 2_000), _holes(400_000, 3_000)]
     packed = [pack_trace(t) for t in traces]
-    offs = np.zeros(3, dtype=np.int64)
+    offs = np.zeros(4, dtype=np.int64)
     np.cumsum([len(p.reqs) for p in packed], out=offs[1:])
     reqs = np.concatenate([p.reqs for p in packed])
     cfg = cfg_record(AllocatorConfig())
     batch = DeviceBatch(reqs, offs, cfg)
     batch.launch()
     got = batch.results()
-    tiers = batch.tier_counts()
+    passes = batch.tier_counts()
     want, _ = oracle.replay_batch(reqs, offs, cfg)
     assert_same(got, want)
-    assert int(want[1]["max_free_blocks"]) >= 240_000
-    assert tiers[2] == 2 and tiers[3] == 1, tiers  # both reach tier 3, one tier 4
+    assert int(want[2]["max_free_blocks"]) >= 400_000
+    assert passes[:2] == [3, 2] and passes[5] == 1, passes

@@ -20,4 +20,4 @@ for _ in range(2):
     t = time.perf_counter(); batch.launch(); torch.cuda.synchronize(); dt = time.perf_counter() - t
     r = batch.results()
     ctl = batch.d_ws[:64].cpu().numpy().view(np.uint32)
-    print(f"{len(reqs)} requests {dt:.2f} s  {len(reqs)/dt/1e6:.2f} Mreq/s tiers {ctl[9:13]} maxF {r['max_free_blocks'][0]} nseg {r['n_segments_peak'][0]} status {r['status'][0]}")
+    print(f"{len(reqs)} requests {dt:.2f} s  {len(reqs)/dt/1e6:.2f} Mreq/s passes {ctl[9:15]} maxF {r['max_free_blocks'][0]} nseg {r['n_segments_peak'][0]} status {r['status'][0]}")
