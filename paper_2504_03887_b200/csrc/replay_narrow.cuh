@@ -77,10 +77,11 @@ struct NPool {
 // Allocated-block records, 16 B per handle: x addr_u, y size_u (0 never
 // allocated, kFreedU freed), z left ref, w right ref.
 struct NRecs {
-  u32* base;
+  uint4* base;
   __device__ __forceinline__ u32* word(u32 h, int w) const {
-    return base + 4 * (size_t)h + w;
+    return reinterpret_cast<u32*>(base + h) + w;  // w: immediate offset
   }
+  __device__ __forceinline__ uint4* rec(u32 h) const { return base + h; }
 };
 
 // Directory in registers: lane d holds bucket position d -- its lower bound
@@ -632,11 +633,19 @@ __device__ __forceinline__ void replay_trace(
   }
 
   NRecs rec;
-  rec.base = rec_base + 4 * (size_t)e0;
-  {
-    uint4* r4 = reinterpret_cast<uint4*>(rec.base);
-    for (long long i = lane; i < n; i += 32) r4[i] = make_uint4(0, 0, 0, 0);
-  }
+  rec.base = reinterpret_cast<uint4*>(rec_base) + e0;
+  // this trace's timeline entries (null: no timeline requested)
+  longlong2* const tl =
+      timeline ? reinterpret_cast<longlong2*>(timeline) + e0 : nullptr;
+  // Handle watermark instead of zeroing the record table: records of
+  // handles <= wm belong to this run (written by an allocation, or zeroed
+  // below); a handle above it has not been touched yet, so its record is
+  // "never allocated" without reading memory.  Interned handles appear in
+  // first-appearance order (pack_trace, wire words), so the watermark
+  // advances without gaps and nothing is zeroed; a gap is zeroed when the
+  // watermark jumps over it.  Retry passes start from their own watermark,
+  // so records left by an earlier pass are never trusted.
+  int wm = -1;
   dir.init(lane);
   __syncwarp();
 
@@ -707,15 +716,35 @@ __device__ __forceinline__ void replay_trace(
     }
     const int my_h = lane < cnt ? (int)lo(cb[lane].y) : -1;
     const bool hok = my_h >= 0 && my_h < n;
+    const bool fresh = hok && my_h > wm;
+    {
+      const int cmax = __reduce_max_sync(kFull, hok ? my_h : -1);
+      if (cmax > wm) {
+        // distinct fresh handles in the chunk; fewer than cmax - wm means
+        // the watermark jumps over handles this chunk does not touch
+        const unsigned same = __match_any_sync(kFull, fresh ? my_h : -1);
+        const bool first = fresh && (same & lanemask_lt()) == 0u;
+        const int distinct = __popc(__ballot_sync(kFull, first));
+        if (distinct < cmax - wm) {
+          for (int h = wm + 1 + lane; h <= cmax; h += 32)
+            *rec.rec((u32)h) = make_uint4(0, 0, 0, 0);
+          __syncwarp();
+        }
+        wm = cmax;
+      }
+    }
     uint4 r = make_uint4(0, 0, 0, 0);
-    if (hok) r = *reinterpret_cast<const uint4*>(rec.word((u32)my_h, 0));
+    if (hok && !fresh) r = *rec.rec((u32)my_h);
     uint4* st = sg.rec;
     st[lane] = r;
     const int hcmp = hok ? my_h : -1;
     __syncwarp();
 
+    ulonglong2 ev_next = cb[0];
     for (int j = 0; j < cnt; ++j) {
-      const ulonglong2 ev = cb[j];
+      // the next request's load is issued before this one's dependent chain
+      const ulonglong2 ev = ev_next;
+      if (j + 1 < cnt) ev_next = cb[j + 1];
       const long long size = (long long)ev.x;
       const int hj = (int)lo(ev.y);
       const unsigned ks = hi(ev.y);
@@ -896,7 +925,7 @@ __device__ __forceinline__ void replay_trace(
             if (lane == j) {
               const uint4 o = make_uint4(out_a, out_s, out_L, out_R);
               st[j] = o;
-              *reinterpret_cast<uint4*>(rec.word((u32)hj, 0)) = o;
+              *rec.rec((u32)hj) = o;
             }
           } else if (lane == j) {
             st[j].y = kFreedU;
@@ -909,8 +938,8 @@ __device__ __forceinline__ void replay_trace(
         stop = cbase + j;
         break;
       }
-      if (timeline != nullptr && lane == j)
-        reinterpret_cast<longlong2*>(timeline)[e0 + (long long)(cbase + j)] =
+      if (tl != nullptr && lane == j)
+        tl[cbase + j] =
             make_longlong2(c.reserved, c.allocated);
       __syncwarp();
     }

@@ -225,3 +225,61 @@ def test_main_kernel_variants_vs_oracle(env):
                          capture_output=True, text=True, timeout=600)
     assert out.returncode == 0, out.stderr[-3000:]
     assert "wide ok" in out.stdout
+
+
+def _permuted_trace(rng, n_allocs):
+    """Raw pm_req_t records whose dense handles are NOT in first-appearance
+    order (the C ABI allows any dense handles), with a few malformed
+    requests: frees of never-allocated handles, double frees, duplicates."""
+    perm = rng.permutation(2 * n_allocs)  # handles < n_requests
+    recs, live, used = [], [], []
+    _permuted_trace.unused = int(perm[n_allocs])  # a handle never allocated
+    for k in range(n_allocs):
+        h = int(perm[k])
+        recs.append((int(rng.integers(1, 64 << 20)), h, 0))
+        live.append(h)
+        used.append(h)
+        while live and rng.random() < 0.45:
+            recs.append((0, live.pop(int(rng.integers(len(live)))), 1))
+    for h in live:
+        recs.append((0, h, 1))
+    out = np.array(recs, dtype=_native.REQ_DTYPE)
+    return out
+
+
+def test_out_of_order_handles_and_dirty_workspace_vs_oracle():
+    # the handle watermark must zero the records it jumps over; a second
+    # launch over the same (dirty) workspace must not trust old records
+    rng = np.random.default_rng(99)
+    traces = [_permuted_trace(rng, m) for m in (3, 40, 700, 5000)]
+    bad = []
+    for kind in range(3):  # unknown handle, double free, duplicate alloc
+        t = _permuted_trace(rng, 300).copy()
+        i = len(t) // 2
+        if kind == 0:
+            h = _permuted_trace.unused
+            t = np.concatenate([t[:i], np.array([(0, h, 1)], t.dtype), t[i:]])
+        elif kind == 1:
+            f = np.nonzero(t["kind_stream"][:i] == 1)[0][-1]
+            t = np.concatenate([t[:i], t[f:f + 1], t[i:]])
+        else:
+            a = np.nonzero(t["kind_stream"][:i] == 0)[0][-1]
+            t = np.concatenate([t[:i], t[a:a + 1], t[i:]])
+        bad.append(t)
+    traces += bad
+    offs = np.zeros(len(traces) + 1, dtype=np.int64)
+    np.cumsum([len(t) for t in traces], out=offs[1:])
+    reqs = np.concatenate(traces)
+    assert (reqs["handle"] < np.repeat(np.diff(offs), np.diff(offs))).all()
+    cfg = cfg_record(AllocatorConfig())
+    want, tl_ref = oracle.replay_batch(reqs, offs, cfg, timeline=True)
+    assert set(want["status"][-3:].tolist()) == {2, 3, 4}
+    from paper_2504_03887_b200.engine import DeviceBatch
+    batch = DeviceBatch(reqs, offs, cfg, timeline=True)
+    for _ in range(2):
+        batch.launch()
+        assert (batch.results() == want).all()
+        tlb = batch.timeline().ravel()
+        assert (tlb[:tl_ref.size] == tl_ref.ravel()).all()
+    got, tl = _native.replay_host(reqs, offs, cfg, None, True)
+    assert (got == want).all() and (tl == tl_ref).all()
