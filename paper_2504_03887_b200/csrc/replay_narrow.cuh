@@ -221,6 +221,7 @@ struct NDir {
     nb = 0;
   }
   __device__ __forceinline__ bool full() const { return nb >= 32; }
+  __device__ __forceinline__ int capacity() const { return 32; }
 };
 
 struct NWarpState;
@@ -388,6 +389,10 @@ __device__ __forceinline__ int pool_insert(const NPool& P, D& dir, NCtx& c,
   int d = dir.find(ka);
   unsigned m = dir.mask(d);
   while (m == kFull) {
+    // a full directory whose buckets are >= 3/4 occupied would thrash
+    // (merge a pair, split, merge ...) on every insert: hand the trace to
+    // the next pass, which has room, instead
+    if (dir.full() && c.F >= 24 * dir.capacity()) return -1;
     if (!split_bucket(P, dir, d, rec, st, hcmp, lane)) return -1;
     d = dir.find(ka);
     m = dir.mask(d);
@@ -593,7 +598,7 @@ __device__ __forceinline__ void replay_trace(
     pm_result_t* __restrict__ results, int64_t* __restrict__ timeline,
     u32* rec_base, const NPool& P, D& dir, NStage& sg, int lane,
     const u64* __restrict__ wire, pm_req_t* __restrict__ expand,
-    bool expand_overflow) {
+    bool expand_overflow, int long_trace) {
   const long long e0 = offs[tr];
   const int n = (int)(offs[tr + 1] - e0);  // < 2^31 (pm_replay_batch)
   const pm_cfg_t* cp = cfgs + (cfg_of ? cfg_of[tr] : 0);
@@ -655,6 +660,11 @@ __device__ __forceinline__ void replay_trace(
   c.ws = ws;
   int status = PM_OK;
   int stop = -1;
+  // A trace of >= 2^20 requests replays at one warp's latency (~1 us per
+  // request) in every pass, and long traces are the ones that outgrow the
+  // earlier passes' capacity and restart: send it straight to the last
+  // narrow pass.
+  const bool skip = n >= long_trace;
 
   // requests arrive as pm_req_t (16 B) or as wire words (8 B, decoded in
   // shared memory below)
@@ -662,7 +672,11 @@ __device__ __forceinline__ void replay_trace(
   // is fetched from the even word at or before it, rounded up to an even
   // count (a word of the neighbouring trace at either end is ignored).
   int abase = 0;  // wire: allocs before this chunk (= the next new handle)
-  const int nchunks = (n + 31) / 32;
+  const int nchunks = skip ? 0 : (n + 31) / 32;
+  if (skip) {
+    status = PM_POOL_OVERFLOW;
+    stop = 0;
+  }
   auto fetch = [&](int k, u32 buf) {
     const int cnt = min(n - 32 * k, 32);
     if (wire) {
@@ -675,7 +689,7 @@ __device__ __forceinline__ void replay_trace(
                 sg.bar + buf);
     }
   };
-  if (lane == 0 && n > 0) fetch(0, sg.g & 1);
+  if (lane == 0 && nchunks > 0) fetch(0, sg.g & 1);
 
   for (int k = 0; k < nchunks; ++k) {
     const int cbase = 32 * k;
@@ -1023,6 +1037,7 @@ __device__ __forceinline__ NStage carve_stage(char* wst) {
 //   3..6 the wide tiers 1-4 of replay_device.cuh            (kTierWide1..)
 // A capacity overflow moves a trace to the next capacity tier; an encoding
 // limit sends it to the first wide tier.
+constexpr int kLongTrace = 1 << 20;  // requests: straight to pass 2
 constexpr int kTierMemSmem = 1;
 constexpr int kTierMemHbm = 2;
 constexpr int kTierWide1 = 3;
@@ -1162,6 +1177,7 @@ struct NDirMem {
   __device__ __forceinline__ void release_all() { nb = 0; }
   __device__ __forceinline__ void release_victim_token() {}
   __device__ __forceinline__ bool full() const { return nb >= nbmax; }
+  __device__ __forceinline__ int capacity() const { return nbmax; }
 };
 
 // Shared memory of a memory-directory tier CTA (one warp): staging, the
@@ -1244,7 +1260,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
     const int tr = list ? list[t] : (int)t;
     if (lane == 0) atomicAdd(active, 1);
     replay_trace(tr, reqs, offs, cfgs, cfg_of, results, timeline, recs, P, dir,
-                 sg, lane, wire, expand, false);
+                 sg, lane, wire, expand, false, kLongTrace);
     __syncwarp();
     if (lane == 0) atomicSub(active, 1);
     const int sts = results[tr].status;
@@ -1303,7 +1319,8 @@ __global__ void __launch_bounds__(32, 1)
     const int tr = list[t];
     // the last narrow tier expands wire words for the wide tier it hands to
     replay_trace(tr, reqs, offs, cfgs, cfg_of, results, timeline, recs, P, dir,
-                 sg, lane, wire, expand, !SMEM_POOL);
+                 sg, lane, wire, expand, !SMEM_POOL,
+                 SMEM_POOL ? kLongTrace : 0x7FFFFFFF);
     __syncwarp();
     if (lane == 0)
       route(ctl, results[tr].status, tr, SMEM_POOL ? kTierMemHbm : kTierWide4,
