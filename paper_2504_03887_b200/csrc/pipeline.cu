@@ -276,15 +276,35 @@ __global__ void k_depth_final(const long long* jump, long long nl, int* depth) {
 }
 
 // subtree sizes, one depth level at a time from the deepest
+// One warp per node of the level: a node's children are read 32 at a time
+// (a wrapper can have hundreds of thousands of them, which one thread would
+// walk serially).
+__device__ __forceinline__ long long warp_sum_ll(long long x) {
+  for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
+  return x;
+}
+__device__ __forceinline__ long long warp_incl_scan_ll(long long x) {
+  const int lane = threadIdx.x & 31;
+  for (int o = 1; o < 32; o <<= 1) {
+    const long long y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  return x;
+}
+
+// subtree sizes, one level at a time from the bottom
 __global__ void k_subtree_level(const long long* lvl_nodes, long long m,
                                 const long long* child_order,
                                 const long long* off, long long* size) {
-  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (i >= m) return;
-  const long long v = lvl_nodes[i];
-  long long s = 1;
-  for (long long k = off[v + 1]; k < off[v + 2]; ++k) s += size[child_order[k]];
-  size[v] = s;
+  const long long w = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= m) return;  // whole warp
+  const long long v = lvl_nodes[w];
+  long long s = 0;
+  for (long long k = off[v + 1] + lane; k < off[v + 2]; k += 32)
+    s += size[child_order[k]];
+  s = warp_sum_ll(s);
+  if (lane == 0) size[v] = s + 1;
 }
 
 // pre-order positions, one level at a time from the top: children of v
@@ -293,14 +313,22 @@ __global__ void k_preorder_level(const long long* lvl_nodes, long long m,
                                  const long long* child_order,
                                  const long long* off, const long long* size,
                                  long long* pre) {
-  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (i >= m) return;
-  const long long v = lvl_nodes[i];  // -1: the synthetic root
+  const long long w = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= m) return;  // whole warp
+  const long long v = lvl_nodes[w];  // -1: the synthetic root
   long long next = v >= 0 ? pre[v] + 1 : 0;
-  for (long long k = off[v + 1]; k < off[v + 2]; ++k) {
-    const long long c = child_order[k];
-    pre[c] = next;
-    next += size[c];
+  const long long b = off[v + 2];
+  for (long long base = off[v + 1]; base < b; base += 32) {
+    const long long k = base + lane;
+    long long c = -1, sz = 0;
+    if (k < b) {
+      c = child_order[k];
+      sz = size[c];
+    }
+    const long long incl = warp_incl_scan_ll(sz);
+    if (k < b) pre[c] = next + incl - sz;
+    next += __shfl_sync(0xffffffffu, incl, 31);
   }
 }
 
@@ -1789,7 +1817,7 @@ int pm_layer_tree(int64_t n, const int64_t* pid, const int64_t* par,
   for (int d = maxd; d >= 0; --d) {
     const long long a = h_lvl[d], b = h_lvl[d + 1];
     if (b > a)
-      pmp::k_subtree_level<<<blocks_for(b - a), 256, 0, s>>>(by_depth + a, b - a,
+      pmp::k_subtree_level<<<blocks_for(32 * (b - a)), 256, 0, s>>>(by_depth + a, b - a,
                                                               ord, off, size);
   }
   const long long m1 = -1;
@@ -1798,7 +1826,7 @@ int pm_layer_tree(int64_t n, const int64_t* pid, const int64_t* par,
   for (int d = 0; d < maxd; ++d) {
     const long long a = h_lvl[d], b = h_lvl[d + 1];
     if (b > a)
-      pmp::k_preorder_level<<<blocks_for(b - a), 256, 0, s>>>(by_depth + a, b - a,
+      pmp::k_preorder_level<<<blocks_for(32 * (b - a)), 256, 0, s>>>(by_depth + a, b - a,
                                                                ord, off, size, pre);
   }
   // reachable nodes: depth >= 0, i.e. by_depth[h_lvl[0] ..]
