@@ -362,13 +362,13 @@ def main():
                      "traffic_note": "GB/s: DRAM read+write bytes per event from the ncu "
                                      "--set full capture (profiles/replay_ncu_summary.json) "
                                      "x events per launch / launch time",
-                     "kernel": "replay_narrow_kernel<24> (main pass, 100 % of GPU time in profiles/r01_v7_bench_launches.csv; the tier-1..4 retry kernels ride in the same timed launch)",
+                     "kernel": "replay_narrow_kernel<24> (main pass, 100 % of GPU time in profiles/r01_v7_bench_launches.csv; the six retry-pass kernels ride in the same timed launch)",
                      "algorithmic_bytes_per_event": BYTES_PER_EVENT},
         "cpu_baseline": cpu,
         "parity": parity,
         "clocks": clocks.summary(),
         "issue_bound": issue,
-        "gpu_launches": 5 * args.steps,  # main pass + 4 retry tiers per pm_replay_batch
+        "gpu_launches": 7 * args.steps,  # main pass + 2 narrow + 4 wide retry passes per pm_replay_batch
     }
     if issue is not None:
         mhz = line["clocks"]["sm_mhz"] or 1965.0
