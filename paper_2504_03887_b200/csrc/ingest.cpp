@@ -26,6 +26,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <unordered_map>
 #include <vector>
 
@@ -50,8 +51,13 @@ struct Cols {
   std::unordered_map<std::string, int32_t> intern;
   std::string names;               // distinct names, UTF-8
   std::vector<int64_t> name_off;   // code-point offsets, n_names+1
+  std::vector<int64_t> name_boff;  // byte offsets into `names`, n_names+1
   int64_t dropped = 0;
   int64_t cp_total = 0;
+  Cols() {
+    name_off.push_back(0);
+    name_boff.push_back(0);
+  }
 };
 
 // ---- JSON scanning -----------------------------------------------------------
@@ -332,6 +338,7 @@ int32_t intern_name(Cols& C, const std::string& s) {
   C.cp_total += n;
   C.names += s;
   C.name_off.push_back(C.cp_total);
+  C.name_boff.push_back((int64_t)C.names.size());
   return id;
 }
 
@@ -548,6 +555,157 @@ struct Out {
   }
 };
 
+// Strict UTF-8 validation (the reference reads the file with
+// encoding="utf-8"; invalid input goes to the Python reader, which raises the
+// reference's error).  ASCII runs are skipped 8 bytes at a time.
+bool valid_utf8(const unsigned char* p, const unsigned char* end) {
+  while (p < end) {
+    if (end - p >= 8) {
+      uint64_t w;
+      memcpy(&w, p, 8);
+      if ((w & 0x8080808080808080ull) == 0) {
+        p += 8;
+        continue;
+      }
+    }
+    const unsigned c = *p;
+    if (c < 0x80) {
+      ++p;
+      continue;
+    }
+    int n;
+    uint32_t cp;
+    if ((c & 0xE0) == 0xC0) { n = 1; cp = c & 0x1F; }
+    else if ((c & 0xF0) == 0xE0) { n = 2; cp = c & 0x0F; }
+    else if ((c & 0xF8) == 0xF0) { n = 3; cp = c & 0x07; }
+    else return false;
+    if (end - p <= n) return false;
+    for (int k = 1; k <= n; ++k) {
+      if ((p[k] & 0xC0) != 0x80) return false;
+      cp = (cp << 6) | (p[k] & 0x3F);
+    }
+    if ((n == 1 && cp < 0x80) || (n == 2 && cp < 0x800) || (n == 3 && cp < 0x10000) ||
+        cp > 0x10FFFF || (cp >= 0xD800 && cp <= 0xDFFF))
+      return false;
+    p += n + 1;
+  }
+  return true;
+}
+
+// Append B's rows to A, re-interning B's names into A's table (B's distinct
+// names in B's first-occurrence order, so A's table order is the order a
+// sequential parse of A's text followed by B's would produce).
+void append_cols(Cols& A, Cols& B) {
+  const size_t nb = B.name_boff.size() - 1;
+  std::vector<int32_t> map(nb);
+  for (size_t k = 0; k < nb; ++k)
+    map[k] = intern_name(A, B.names.substr((size_t)B.name_boff[k],
+                                           (size_t)(B.name_boff[k + 1] - B.name_boff[k])));
+  A.ts.insert(A.ts.end(), B.ts.begin(), B.ts.end());
+  A.dur.insert(A.dur.end(), B.dur.begin(), B.dur.end());
+  A.cat.insert(A.cat.end(), B.cat.begin(), B.cat.end());
+  for (int f = 0; f < F_N; ++f)
+    A.ints[f].insert(A.ints[f].end(), B.ints[f].begin(), B.ints[f].end());
+  A.name_id.reserve(A.name_id.size() + B.name_id.size());
+  for (int32_t id : B.name_id) A.name_id.push_back(map[id]);
+  A.dropped += B.dropped;
+}
+
+// The records of a JSON array, P.p just past its '['.  Large arrays are cut
+// into chunks that start at "\n  {" (how profilers lay records out), parsed
+// by one thread each; chunk t must stop exactly where chunk t+1 starts and
+// the last must reach the ']' -- otherwise (a cut inside a record, an
+// unsupported construct) the sequential loop below reparses the array, so
+// the result is the sequential parse's either way.
+void parse_records(Parser& P, Cols& C, bool strict) {
+  const char* begin = P.p;
+  const size_t len = (size_t)(P.end - begin);
+  unsigned T = std::thread::hardware_concurrency();
+  if (T > 16) T = 16;
+  if (len / T < (1u << 20)) T = (unsigned)(len >> 20);
+  // records are laid out like the first one: a newline, its indentation,
+  // '{' (profilers: "\n  {"); a first record not on its own line gives no
+  // cut points
+  std::string pat;
+  const char* first = begin;
+  while (first < P.end && (*first == ' ' || *first == '\n' || *first == '\r' ||
+                           *first == '\t'))
+    ++first;
+  if (T >= 2 && first < P.end && *first == '{') {
+    const char* nl = first;
+    while (nl > begin && nl[-1] != '\n') --nl;
+    if (nl > begin) pat = "\n" + std::string(nl, first) + "{";
+  }
+  std::vector<const char*> start{first};
+  if (!pat.empty()) {
+    for (unsigned t = 1; t < T; ++t) {
+      const char* b = begin + len * t / T;
+      const char* q = static_cast<const char*>(
+          memmem(b, (size_t)(P.end - b), pat.data(), pat.size()));
+      if (q && q + pat.size() - 1 > start.back()) start.push_back(q + pat.size() - 1);
+    }
+  }
+  if (start.size() >= 2) {
+    const size_t nt = start.size();
+    std::vector<Cols> part(nt);
+    std::vector<const char*> stop(nt, nullptr);
+    std::vector<char> closed(nt, 0), ok(nt, 0);
+    auto work = [&](size_t t) {
+      try {
+        Parser Q{start[t], P.end};
+        const char* next = t + 1 < nt ? start[t + 1] : nullptr;
+        if (Q.peek() == ']') {  // empty array
+          ++Q.p;
+          closed[t] = 1;
+          stop[t] = Q.p;
+          ok[t] = 1;
+          return;
+        }
+        while (true) {
+          record(Q, part[t], strict);
+          const char d = Q.peek();
+          ++Q.p;
+          if (d == ']') {
+            closed[t] = 1;
+            break;
+          }
+          if (d != ',') return;
+          Q.ws();
+          if (next && Q.p >= next) break;
+        }
+        stop[t] = Q.p;
+        ok[t] = 1;
+      } catch (...) {
+      }
+    };
+    std::vector<std::thread> th;
+    for (size_t t = 1; t < nt; ++t) th.emplace_back(work, t);
+    work(0);
+    for (auto& x : th) x.join();
+    bool good = true;
+    for (size_t t = 0; t < nt && good; ++t) {
+      good = ok[t] && (t + 1 < nt ? (!closed[t] && stop[t] == start[t + 1]) : closed[t]);
+    }
+    if (good) {
+      for (size_t t = 0; t < nt; ++t) append_cols(C, part[t]);
+      P.p = stop[nt - 1];
+      return;
+    }
+  }
+  // sequential
+  if (P.peek() == ']') {
+    ++P.p;
+    return;
+  }
+  while (true) {
+    record(P, C, strict);
+    const char d = P.peek();
+    ++P.p;
+    if (d == ']') break;
+    if (d != ',') throw Unsupported();
+  }
+}
+
 }  // namespace
 
 extern "C" {
@@ -558,8 +716,12 @@ const char* pm_ingest_last_error(void) { return g_err.c_str(); }
 // PM_INGEST_UNSUPPORTED (5: use the Python reader) or PM_INGEST_EMPTY (7).
 int pm_ingest_json(const char* text, int64_t len, int strict, void** handle) {
   *handle = nullptr;
+  if (!valid_utf8(reinterpret_cast<const unsigned char*>(text),
+                  reinterpret_cast<const unsigned char*>(text) + len)) {
+    g_err = "input is not valid UTF-8";
+    return PM_INGEST_UNSUPPORTED;
+  }
   Cols* C = new Cols();
-  C->name_off.push_back(0);
   Parser P{text, text + len};
   try {
     const char c = P.peek();
@@ -574,17 +736,7 @@ int pm_ingest_json(const char* text, int64_t len, int strict, void** handle) {
             if (found) throw Unsupported();  // duplicate key: last wins, rare
             found = true;
             P.expect('[');
-            if (P.peek() == ']') {
-              ++P.p;
-            } else {
-              while (true) {
-                record(P, *C, strict != 0);
-                const char d = P.peek();
-                ++P.p;
-                if (d == ']') break;
-                if (d != ',') throw Unsupported();
-              }
-            }
+            parse_records(P, *C, strict != 0);
           } else {
             P.skip();
           }
@@ -599,17 +751,7 @@ int pm_ingest_json(const char* text, int64_t len, int strict, void** handle) {
       if (!found) throw Unsupported();
     } else if (c == '[') {
       ++P.p;
-      if (P.peek() == ']') {
-        ++P.p;
-      } else {
-        while (true) {
-          record(P, *C, strict != 0);
-          const char d = P.peek();
-          ++P.p;
-          if (d == ']') break;
-          if (d != ',') throw Unsupported();
-        }
-      }
+      parse_records(P, *C, strict != 0);
     } else {
       throw Unsupported();
     }

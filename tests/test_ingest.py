@@ -287,3 +287,49 @@ def test_digest_synthetic_name_view():
     est = PeakMemoryEstimator()
     assert _ingest.bundle_digest(b, b.metadata, 2, 1 << 36, 0, None) == \
         est._digest_json(b, 1 << 36, 0)
+
+
+# ---- the parallel chunked parse of large arrays ------------------------------
+
+def _big_records(seed, n):
+    rng = random.Random(seed)
+    return [_clean_record(rng, i) for i in range(n)]
+
+
+@pytest.mark.parametrize("layout", ["torch", "compact", "nested_at_cut", "trailing_keys",
+                                    "top_level_array"])
+def test_parallel_chunks_equal_python(layout):
+    # > 2 MB per document so the reader cuts the array into chunks; every
+    # layout must give the sequential (Python-reader) columns: cuts at
+    # record starts are taken, cuts that land inside a record or find no
+    # record start fall back to the sequential parse
+    recs = _big_records(77, 40_000)
+    if layout == "torch":  # profiler layout: records at "\n  {"
+        text = json.dumps({"schemaVersion": 1, "traceEvents": recs}, indent=2)
+    elif layout == "compact":  # one line: no cut point at all
+        text = json.dumps({"traceEvents": recs})
+    elif layout == "nested_at_cut":  # "\n  {" inside records too
+        body = ",".join("\n  {\n\"x\": \n  {\"y\": 1},\n" + json.dumps(r)[1:] for r in recs)
+        text = '{"traceEvents": [' + body + "\n]}"
+    elif layout == "trailing_keys":
+        text = json.dumps({"traceEvents": recs, "after": [{"a": 1}] * 3000,
+                           "z": {"q": 2}}, indent=2)
+    else:
+        text = json.dumps(recs, indent=2)
+    assert len(text) > 4 << 20
+    got = _ingest.parse_json(text.encode("utf-8"), False)
+    assert isinstance(got, tuple), layout
+    assert_same(got, text)
+
+
+def test_invalid_utf8_declined_and_parse_trace_raises(tmp_path):
+    from paper_2504_03887_b200.trace import parse_trace
+    good = json.dumps({"traceEvents": [{"ph": "X", "cat": "cpu_op", "name": "é",
+                                        "ts": 1, "dur": 2}]}).encode("utf-8")
+    for bad in (good.replace(b"\\u00e9", b"\xc3"), good + b"\xff", b"\xef\xbb\xbf" + good,
+                good.replace(b"\\u00e9", b"\xed\xa0\x80")):  # lone surrogate
+        assert _ingest.parse_json(bad, False) == _ingest.UNSUPPORTED
+    f = tmp_path / "t.json"
+    f.write_bytes(good.replace(b"\\u00e9", b"\xc3"))
+    with pytest.raises(MalformedTrace, match="not valid JSON"):
+        parse_trace(f)
