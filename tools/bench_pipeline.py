@@ -69,7 +69,9 @@ def main():
             from paper_2504_03887_b200.trace import parse_trace
             with tempfile.TemporaryDirectory() as d:
                 path = Path(d) / "c5.trace.json"
-                path.write_text(json.dumps(b.to_json_dict()))
+                # laid out like a profiler's chrome trace: one record per
+                # indented block (the torch profiler writes "\n  {" blocks)
+                path.write_text(json.dumps(b.to_json_dict(), indent=2))
                 line["file_mb"] = path.stat().st_size / 1e6
                 tf = time.perf_counter()
                 pb = parse_trace(path, b.metadata)
