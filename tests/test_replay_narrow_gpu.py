@@ -283,3 +283,55 @@ def test_out_of_order_handles_and_dirty_workspace_vs_oracle():
         assert (tlb[:tl_ref.size] == tl_ref.ravel()).all()
     got, tl = _native.replay_host(reqs, offs, cfg, None, True)
     assert (got == want).all() and (tl == tl_ref).all()
+
+
+@pytest.mark.parametrize("host_copy", ["0", "1"])
+def test_pinned_host_buffers_zero_copy_and_streamed(host_copy, monkeypatch):
+    # pinned requests are read in place by the kernel (zero copy) or, with
+    # PM_HOST_COPY=1, streamed by the copy engines behind the launched main
+    # pass; both entry points, full timelines, vs the oracle
+    import torch
+    monkeypatch.setenv("PM_HOST_COPY", host_copy)
+    reqs, offs = synth.generate(40, first=7000)
+    cfgs = np.concatenate([cfg_record(AllocatorConfig()),
+                           cfg_record(AllocatorConfig(max_split_size=64 * MIB,
+                                                      device_capacity=24 * GIB))])
+    cof = (np.arange(40) % 2).astype(np.int32)
+    pin = torch.empty(len(reqs) * 16, dtype=torch.uint8, pin_memory=True)
+    preqs = pin.numpy().view(_native.REQ_DTYPE)
+    preqs[:] = reqs
+    wpin = torch.empty(len(reqs) * 8, dtype=torch.uint8, pin_memory=True)
+    words = _native.wire_pack(preqs, offs, out=wpin.numpy().view(np.uint64))
+    want, tl_ref = oracle.replay_batch(reqs, offs, cfgs, cof, timeline=True)
+    got, tl = _native.replay_host(preqs, offs, cfgs, cof, True)
+    assert (got == want).all() and (tl == tl_ref).all()
+    got, tl = _native.replay_host_wire(words, offs, cfgs, cof, True)
+    assert (got == want).all() and (tl == tl_ref).all()
+
+
+_STARVED_SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, {repo!r}); sys.path.insert(0, {tests!r})
+from oracle import replay as oracle
+from paper_2504_03887_b200 import _native, synth
+from paper_2504_03887_b200.allocator import AllocatorConfig, cfg_record
+from paper_2504_03887_b200.engine import DeviceBatch
+reqs, offs = synth.generate(300, first=2000)
+cfg = cfg_record(AllocatorConfig())
+want, _ = oracle.replay_batch(reqs, offs, cfg)
+b = DeviceBatch(reqs, offs, cfg)
+b.launch()
+assert (b.results() == want).all()
+print("starved ok", b.tier_counts())
+"""
+
+
+def test_starved_shared_pool_waits_and_escalates_vs_oracle():
+    # a 48-bucket pool for 24 warps: warps wait for buckets, deadlocked CTAs
+    # give up one victim at a time; every result must still be the oracle's
+    code = _STARVED_SCRIPT.format(repo=str(REPO), tests=str(REPO / "tests"))
+    out = subprocess.run([sys.executable, "-c", code],
+                         env={**os.environ, "PM_POOL_BUCKETS": "48"},
+                         capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-3000:]
+    assert "starved ok" in out.stdout
