@@ -234,12 +234,13 @@ struct NCtx {
 // Per-trace values read only on the allocation / segment paths live in the
 // warp's shared staging area rather than in registers (registers set how
 // many warps fit per SM).
-struct NWarpState {
-  const pm_cfg_t* cp;
+struct __align__(16) NWarpState {
+  // read together (one 128-bit load) at the top of every request
   u32 amask;      // alignment - 1 (bytes; alignment <= 2^31 in this pass)
   u32 lim;        // largest rounded request in units (0: unit too large)
   u32 span;       // best-fit window in units (0xFFFFFFFF: unbounded)
   u32 split_lim;  // splittable iff size_u <= split_lim
+  const pm_cfg_t* cp;
   long long peak_reserved, peak_allocated;
   u32 next_base;  // units
   int nseg, nseg_peak, maxF;  // maxF: free-block high-water mark
@@ -772,6 +773,9 @@ __device__ __forceinline__ void replay_trace(
         sts = PM_BAD_HANDLE;
       } else {
         const uint4 rj = st[src];
+        // the allocation constants, loaded alongside the record
+        const uint4 kc = *reinterpret_cast<const uint4*>(ws);
+        const u32 k_amask = kc.x, k_lim = kc.y, k_span = kc.z, k_split = kc.w;
         int rm_id = -1;
         bool up = false;
         int up_id = -1;
@@ -791,13 +795,12 @@ __device__ __forceinline__ void replay_trace(
           } else if (size <= 0) {
             sts = PM_ZERO_SIZE;
           } else if ((ks >> 2) != 0u ||
-                     ((((u64)size + ws->amask) & ~(u64)ws->amask) >> s) >
-                         (u64)ws->lim) {
+                     ((((u64)size + k_amask) & ~(u64)k_amask) >> s) > (u64)k_lim) {
             sts = PM_ENCODING_LIMIT;  // outside the encoding: wide tiers
           } else {
-            const u32 ru = (u32)((((u64)size + ws->amask) & ~(u64)ws->amask) >> s);
-            const u32 split_lim = ws->split_lim;
-            const int id = best_fit(P, dir, ru, ws->span, lane);
+            const u32 ru = (u32)((((u64)size + k_amask) & ~(u64)k_amask) >> s);
+            const u32 split_lim = k_split;
+            const int id = best_fit(P, dir, ru, k_span, lane);
             if (id >= 0) {
               // hit: _take (allocator.py:234-242), _split (:223-232)
               const u64 KA = P.ka[id];
