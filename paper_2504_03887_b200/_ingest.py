@@ -26,7 +26,7 @@ def load():
         lib = ctypes.CDLL(str(LIB_PATH))
         vp, i64 = ctypes.c_void_p, ctypes.c_int64
         lib.pm_ingest_json.restype = ctypes.c_int
-        lib.pm_ingest_json.argtypes = [ctypes.c_char_p, i64, ctypes.c_int,
+        lib.pm_ingest_json.argtypes = [vp, i64, ctypes.c_int,
                                        ctypes.POINTER(vp)]
         for f in ("pm_ingest_count", "pm_ingest_dropped", "pm_ingest_n_names",
                   "pm_ingest_names_bytes"):
@@ -51,7 +51,10 @@ def parse_json(data: bytes, strict: bool):
     from .trace import NameColumn
     lib = load()
     h = ctypes.c_void_p()
-    rc = lib.pm_ingest_json(data, len(data), 1 if strict else 0, ctypes.byref(h))
+    # any contiguous buffer (bytes, a read-only mmap of the file)
+    buf = np.frombuffer(data, dtype=np.uint8) if len(data) else np.zeros(1, np.uint8)
+    rc = lib.pm_ingest_json(ctypes.c_void_p(buf.ctypes.data), len(data),
+                            1 if strict else 0, ctypes.byref(h))
     if rc != 0:
         return rc
     try:

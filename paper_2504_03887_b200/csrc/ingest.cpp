@@ -54,9 +54,19 @@ struct Cols {
   std::vector<int64_t> name_boff;  // byte offsets into `names`, n_names+1
   int64_t dropped = 0;
   int64_t cp_total = 0;
+  // rows parsed by the chunk threads, kept as they are (copied out in
+  // parallel by pm_ingest_columns) with their name ids mapped into this
+  // table: part k's rows follow this object's own rows and part k-1's
+  std::vector<Cols> parts;
+  std::vector<std::vector<int32_t>> remap;
   Cols() {
     name_off.push_back(0);
     name_boff.push_back(0);
+  }
+  int64_t rows() const {
+    int64_t n = (int64_t)ts.size();
+    for (const Cols& p : parts) n += (int64_t)p.ts.size();
+    return n;
   }
 };
 
@@ -592,23 +602,44 @@ bool valid_utf8(const unsigned char* p, const unsigned char* end) {
   return true;
 }
 
-// Append B's rows to A, re-interning B's names into A's table (B's distinct
-// names in B's first-occurrence order, so A's table order is the order a
-// sequential parse of A's text followed by B's would produce).
-void append_cols(Cols& A, Cols& B) {
+// Adopt B as A's next part: B's distinct names are interned into A's table
+// in B's first-occurrence order (so A's table is the one a sequential parse
+// of A's text followed by B's would build); B's rows stay where they are.
+void adopt_part(Cols& A, Cols&& B) {
   const size_t nb = B.name_boff.size() - 1;
   std::vector<int32_t> map(nb);
   for (size_t k = 0; k < nb; ++k)
     map[k] = intern_name(A, B.names.substr((size_t)B.name_boff[k],
                                            (size_t)(B.name_boff[k + 1] - B.name_boff[k])));
-  A.ts.insert(A.ts.end(), B.ts.begin(), B.ts.end());
-  A.dur.insert(A.dur.end(), B.dur.begin(), B.dur.end());
-  A.cat.insert(A.cat.end(), B.cat.begin(), B.cat.end());
-  for (int f = 0; f < F_N; ++f)
-    A.ints[f].insert(A.ints[f].end(), B.ints[f].begin(), B.ints[f].end());
-  A.name_id.reserve(A.name_id.size() + B.name_id.size());
-  for (int32_t id : B.name_id) A.name_id.push_back(map[id]);
   A.dropped += B.dropped;
+  A.parts.push_back(std::move(B));
+  A.remap.push_back(std::move(map));
+}
+
+// Parallel strict UTF-8 check: the text is cut at T points moved forward
+// to a byte that starts a sequence (UTF-8 resynchronises there).
+bool valid_utf8_parallel(const unsigned char* p, const unsigned char* end) {
+  const size_t len = (size_t)(end - p);
+  unsigned T = std::thread::hardware_concurrency();
+  if (T > 16) T = 16;
+  if (len / T < (4u << 20)) T = (unsigned)(len >> 22);
+  if (T < 2) return valid_utf8(p, end);
+  std::vector<const unsigned char*> cut{p};
+  for (unsigned t = 1; t < T; ++t) {
+    const unsigned char* q = p + len * t / T;
+    while (q < end && (*q & 0xC0) == 0x80) ++q;
+    cut.push_back(q);
+  }
+  cut.push_back(end);
+  std::vector<char> ok(T, 0);
+  std::vector<std::thread> th;
+  for (unsigned t = 1; t < T; ++t)
+    th.emplace_back([&, t] { ok[t] = valid_utf8(cut[t], cut[t + 1]); });
+  ok[0] = valid_utf8(cut[0], cut[1]);
+  for (auto& x : th) x.join();
+  for (char o : ok)
+    if (!o) return false;
+  return true;
 }
 
 // The records of a JSON array, P.p just past its '['.  Large arrays are cut
@@ -687,7 +718,7 @@ void parse_records(Parser& P, Cols& C, bool strict) {
       good = ok[t] && (t + 1 < nt ? (!closed[t] && stop[t] == start[t + 1]) : closed[t]);
     }
     if (good) {
-      for (size_t t = 0; t < nt; ++t) append_cols(C, part[t]);
+      for (size_t t = 0; t < nt; ++t) adopt_part(C, std::move(part[t]));
       P.p = stop[nt - 1];
       return;
     }
@@ -716,8 +747,8 @@ const char* pm_ingest_last_error(void) { return g_err.c_str(); }
 // PM_INGEST_UNSUPPORTED (5: use the Python reader) or PM_INGEST_EMPTY (7).
 int pm_ingest_json(const char* text, int64_t len, int strict, void** handle) {
   *handle = nullptr;
-  if (!valid_utf8(reinterpret_cast<const unsigned char*>(text),
-                  reinterpret_cast<const unsigned char*>(text) + len)) {
+  if (!valid_utf8_parallel(reinterpret_cast<const unsigned char*>(text),
+                           reinterpret_cast<const unsigned char*>(text) + len)) {
     g_err = "input is not valid UTF-8";
     return PM_INGEST_UNSUPPORTED;
   }
@@ -762,7 +793,7 @@ int pm_ingest_json(const char* text, int64_t len, int strict, void** handle) {
     g_err = "outside the native reader's subset";
     return PM_INGEST_UNSUPPORTED;
   }
-  if (C->ts.empty()) {
+  if (C->rows() == 0) {
     delete C;
     return PM_INGEST_EMPTY;
   }
@@ -770,7 +801,7 @@ int pm_ingest_json(const char* text, int64_t len, int strict, void** handle) {
   return PM_INGEST_OK;
 }
 
-int64_t pm_ingest_count(void* h) { return (int64_t)static_cast<Cols*>(h)->ts.size(); }
+int64_t pm_ingest_count(void* h) { return static_cast<Cols*>(h)->rows(); }
 int64_t pm_ingest_dropped(void* h) { return static_cast<Cols*>(h)->dropped; }
 int64_t pm_ingest_n_names(void* h) { return (int64_t)static_cast<Cols*>(h)->intern.size(); }
 int64_t pm_ingest_names_bytes(void* h) { return (int64_t)static_cast<Cols*>(h)->names.size(); }
@@ -782,12 +813,30 @@ void pm_ingest_columns(void* h, double* ts, double* dur, int8_t* cat,
                        int64_t* ints, int32_t* name_id, int64_t* name_off,
                        char* names) {
   Cols* C = static_cast<Cols*>(h);
-  const size_t n = C->ts.size();
-  memcpy(ts, C->ts.data(), n * sizeof(double));
-  memcpy(dur, C->dur.data(), n * sizeof(double));
-  memcpy(cat, C->cat.data(), n);
-  for (int f = 0; f < F_N; ++f) memcpy(ints + f * n, C->ints[f].data(), n * sizeof(int64_t));
-  memcpy(name_id, C->name_id.data(), n * sizeof(int32_t));
+  const size_t n = (size_t)C->rows();
+  // one copy job per row block (this object's own rows, then each part),
+  // run in parallel; part name ids are mapped into the merged table
+  auto copy_block = [&](const Cols& B, size_t at, const std::vector<int32_t>* map) {
+    const size_t m = B.ts.size();
+    memcpy(ts + at, B.ts.data(), m * sizeof(double));
+    memcpy(dur + at, B.dur.data(), m * sizeof(double));
+    memcpy(cat + at, B.cat.data(), m);
+    for (int f = 0; f < F_N; ++f)
+      memcpy(ints + f * n + at, B.ints[f].data(), m * sizeof(int64_t));
+    if (map) {
+      for (size_t i = 0; i < m; ++i) name_id[at + i] = (*map)[B.name_id[i]];
+    } else {
+      memcpy(name_id + at, B.name_id.data(), m * sizeof(int32_t));
+    }
+  };
+  std::vector<std::thread> th;
+  size_t at = C->ts.size();
+  for (size_t k = 0; k < C->parts.size(); ++k) {
+    th.emplace_back(copy_block, std::cref(C->parts[k]), at, &C->remap[k]);
+    at += C->parts[k].ts.size();
+  }
+  copy_block(*C, 0, nullptr);
+  for (auto& x : th) x.join();
   memcpy(name_off, C->name_off.data(), C->name_off.size() * sizeof(int64_t));
   memcpy(names, C->names.data(), C->names.size());
 }
