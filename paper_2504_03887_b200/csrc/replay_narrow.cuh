@@ -457,7 +457,8 @@ __device__ __forceinline__ int pool_upsert(const NPool& P, D& dir, NCtx& c,
 // when the first holds none.
 template <class D>
 __device__ __forceinline__ int best_fit(const NPool& P, const D& dir,
-                                        u32 ru, u32 span, int lane) {
+                                        u32 ru, u32 span, int lane,
+                                        u64& KA, u64& LN) {
   if (dir.nb == 0) return -1;
   const int d = dir.find((u64)ru << 32);
   const int p = dir.phys(d);
@@ -465,17 +466,31 @@ __device__ __forceinline__ int best_fit(const NPool& P, const D& dir,
   const bool has_next = d + 1 < dir.nb;
   const int p2 = dir.phys(d + 1);
   const bool in2 = has_next && ((dir.mask(d + 1) >> lane) & 1u);
+  // both buckets' keys and links in one round of loads: the winner's
+  // entry is then shuffled out, not re-read (an L2 round trip when the
+  // entries live in HBM)
   const u64 ka = in ? P.ka[p * kBucket + lane] : ~0ull;
   const u64 ka2 = in2 ? P.ka[p2 * kBucket + lane] : ~0ull;
+  const u64 ln = in ? P.ln[p * kBucket + lane] : 0ull;
+  const u64 ln2 = in2 ? P.ln[p2 * kBucket + lane] : 0ull;
   PM_STAT(8);
   const bool el = in && hi(ka) >= ru && hi(ka) - ru < span;
   const int w = argmin_pk(el, ka);
-  if (w >= 0) return p * kBucket + w;
+  if (w >= 0) {
+    KA = __shfl_sync(kFull, ka, w);
+    LN = __shfl_sync(kFull, ln, w);
+    return p * kBucket + w;
+  }
   PM_STAT(9);
   const int w2 = argmin_pk(in2, ka2);
   if (w2 >= 0) {
     const u64 kw = __shfl_sync(kFull, ka2, w2);
-    if (hi(kw) - ru < span) return p2 * kBucket + w2;
+    const u64 lw = __shfl_sync(kFull, ln2, w2);
+    if (hi(kw) - ru < span) {
+      KA = kw;
+      LN = lw;
+      return p2 * kBucket + w2;
+    }
   }
   return -1;
 }
@@ -800,11 +815,10 @@ __device__ __forceinline__ void replay_trace(
           } else {
             const u32 ru = (u32)((((u64)size + k_amask) & ~(u64)k_amask) >> s);
             const u32 split_lim = k_split;
-            const int id = best_fit(P, dir, ru, k_span, lane);
+            u64 KA = 0, Lk = 0;
+            const int id = best_fit(P, dir, ru, k_span, lane, KA, Lk);
             if (id >= 0) {
               // hit: _take (allocator.py:234-242), _split (:223-232)
-              const u64 KA = P.ka[id];
-              const u64 Lk = P.ln[id];
               const u32 Lf = lo(Lk), Rf = hi(Lk);
               const u32 S = hi(KA), A = lo(KA);
               out_a = A;
