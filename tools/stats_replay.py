@@ -28,7 +28,14 @@ def main():
     lib = _native.load_library(out)
     _native._lib = lib
     n = int(sys.argv[1]) if len(sys.argv) > 1 else 300
-    reqs, offs = synth.generate(n)
+    if n < 0:  # C5: one event-level trace of -n leaves, orchestrated
+        import paper_2504_03887_b200 as api
+        from paper_2504_03887_b200 import synth_events
+        seq = api.build_sequence(api.analyze(synth_events.generate(-n, 2)), 2)
+        reqs = seq.packed
+        offs = np.array([0, len(reqs)], dtype=np.int64)
+    else:
+        reqs, offs = synth.generate(n)
     res, _ = _native.replay_host(reqs, offs, cfg_record(AllocatorConfig()), None, False)
     st = (ctypes.c_ulonglong * 16)()
     lib.pm_debug_stats(st)
