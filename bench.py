@@ -362,7 +362,7 @@ def main():
                      "traffic_note": "GB/s: DRAM read+write bytes per event from the ncu "
                                      "--set full capture (profiles/replay_ncu_summary.json) "
                                      "x events per launch / launch time",
-                     "kernel": "replay_narrow_kernel<24> (main pass, 100 % of GPU time in profiles/r01_v7_bench_launches.csv; the six retry-pass kernels ride in the same timed launch)",
+                     "kernel": "replay_narrow_kernel<24> (main pass, 100 % of GPU time in profiles/r01_v8_bench_launches.csv; the six retry-pass kernels ride in the same timed launch)",
                      "algorithmic_bytes_per_event": BYTES_PER_EVENT},
         "cpu_baseline": cpu,
         "parity": parity,
