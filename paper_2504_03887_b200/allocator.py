@@ -149,10 +149,11 @@ def pack_trace(requests: Iterable[dict]) -> PackedTrace:
     """
     reqs = list(requests)
     n = len(reqs)
-    out = np.zeros(n, dtype=REQ_DTYPE)
-    sizes = out["size"]
-    handles = out["handle"]
-    ks = out["kind_stream"]
+    # Python lists per column, written into the packed records at the end
+    # (element-wise numpy writes cost more than the reference's replay)
+    sizes = [0] * n
+    handles = [0] * n
+    ks = [0] * n
     seq_nos: list = [None] * n
     host_errors: dict[int, BaseException] = {}
     kinds_raw: dict[int, object] = {}
@@ -192,6 +193,11 @@ def pack_trace(requests: Iterable[dict]) -> PackedTrace:
         except Exception as exc:  # surfaced when (if) replay reaches i
             host_errors[i] = exc
             ks[i] = KIND_MISSING
+    out = np.zeros(n, dtype=REQ_DTYPE)
+    if n:
+        out["size"] = sizes
+        out["handle"] = handles
+        out["kind_stream"] = ks
     return PackedTrace(out, seq_nos, host_errors, kinds_raw)
 
 
