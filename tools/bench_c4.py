@@ -50,7 +50,10 @@ def main():
     line = {"workload": "C4", "traces": len(offs) - 1, "configs": len(cfgs),
             "replays": len(boffs) - 1, "requests": ev, "seconds": min(times),
             "events_per_s": ev / min(times),
-            "statuses": sorted(set(res["status"].tolist()))}
+            "statuses": sorted(set(res["status"].tolist())),
+            "retry_passes": b.tier_counts(),
+            "max_free_blocks": int(res["max_free_blocks"].max()),
+            "longest_trace": int(np.diff(boffs).max())}
     if args.check:
         from oracle import replay as oracle
         t0 = time.perf_counter()
