@@ -1082,18 +1082,35 @@ struct NDirMem {
   int* pos;         // [nbmax] position by physical bucket
   int* pstack;      // [nbmax] free physical buckets
   int nb, ptop, nbmax, lane;
+  // register summary: lane L holds the bounds at positions 32 L and
+  // 32 (L + 32)
+  u64 sb, sb2;
 
+  __device__ __forceinline__ void refresh() {
+    sb = 32 * lane < nb ? db[32 * lane] : ~0ull;
+    sb2 = 32 * (lane + 32) < nb ? db[32 * (lane + 32)] : ~0ull;
+  }
   __device__ __forceinline__ void init(int lane_) {
     lane = lane_;
     nb = 0;
+    sb = sb2 = ~0ull;
     __syncwarp();
     for (int i = lane; i < nbmax; i += 32) pstack[i] = nbmax - 1 - i;
     __syncwarp();
     ptop = nbmax;
   }
-  // last position whose bound <= x: each round probes 32 evenly spaced
-  // positions of the live range, shrinking it 32x
+  // last position whose bound <= x.  Up to 2048 positions: the summary
+  // picks the block of 32, one probe of it the position; beyond, each round
+  // probes 32 evenly spaced positions of the live range, shrinking it 32x
   __device__ __forceinline__ int find(u64 x) const {
+    if (nb <= 2048) {
+      const unsigned hi_b = __ballot_sync(kFull, sb2 <= x);
+      const int blk = hi_b ? 63 - __clz(hi_b)
+                           : 31 - __clz(__ballot_sync(kFull, sb <= x));
+      const int e = 32 * blk + lane;
+      const unsigned b = __ballot_sync(kFull, e < nb && db[e] <= x);
+      return 32 * blk + 31 - __clz(b);
+    }
     int lo_ = 0, hi_ = nb;
     while (hi_ - lo_ > 32) {
       const int step = (hi_ - lo_ + 31) / 32;
@@ -1156,6 +1173,7 @@ struct NDirMem {
     pos[p] = d;
     __syncwarp();
     nb += 1;
+    refresh();
   }
   __device__ __forceinline__ void erase(int d) {
     for (int base = 0; d + 1 + base < nb; base += 32) {
@@ -1178,6 +1196,7 @@ struct NDirMem {
     nb -= 1;
     if (d == 0) db[0] = 0;  // uniform store
     __syncwarp();
+    refresh();
   }
   __device__ __forceinline__ int alloc_phys() {
     if (ptop == 0) return -1;
@@ -1191,7 +1210,10 @@ struct NDirMem {
     __syncwarp();
     ptop += 1;
   }
-  __device__ __forceinline__ void release_all() { nb = 0; }
+  __device__ __forceinline__ void release_all() {
+    nb = 0;
+    sb = sb2 = ~0ull;
+  }
   __device__ __forceinline__ void release_victim_token() {}
   __device__ __forceinline__ bool full() const { return nb >= nbmax; }
   __device__ __forceinline__ int capacity() const { return nbmax; }
