@@ -433,10 +433,53 @@ def run_reference(args, rank, world):
         "e2e": {"value": value, "unit": "events/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
         "implementation": "oracle/replay_oracle.c: C restatement of "
-                          "peakmem.allocator (reference is pure Python, "
-                          "absent on the GPU box)",
+                          "peakmem.allocator (the reference is pure Python; "
+                          "its own throughput is reported beside it)",
     }
+    py = reference_python_rate(reqs, offs, threads)
+    if py is not None:
+        line["reference_python"] = py
     print(json.dumps(line))
+
+
+def _py_replay_worker(args):
+    """One trace through the reference's own replay (baseline/_ref)."""
+    root, recs = args
+    sys.path.insert(0, root)
+    import time as _t
+    from peakmem.allocator import AllocatorConfig as RC, replay as rreplay
+    t0 = _t.perf_counter()
+    rreplay(recs, RC())
+    return len(recs), _t.perf_counter() - t0
+
+
+def reference_python_rate(reqs, offs, threads, n_traces=16):
+    """The reference's own Python replay (peakmem.allocator.replay from the
+    pip-installed baseline/_ref) on the first few sampled traces, one
+    process per trace over all host cores: context for the C port above."""
+    root = REPO / "baseline" / "_ref"
+    if not (root / "peakmem").exists():
+        return None
+    import multiprocessing as mp
+    jobs = []
+    for t in range(min(n_traces, len(offs) - 1)):
+        r = reqs[offs[t]:offs[t + 1]]
+        kinds = ("alloc", "free")
+        recs = [{"seq_no": i, "kind": kinds[int(k) & 3], "block_id": int(h),
+                 "size": int(sz)} for i, (sz, h, k) in
+                enumerate(zip(r["size"].tolist(), r["handle"].tolist(),
+                              r["kind_stream"].tolist()))]
+        jobs.append((str(root), recs))
+    t0 = time.perf_counter()
+    with mp.get_context("fork").Pool(threads) as pool:
+        out = pool.map(_py_replay_worker, jobs)
+    wall = time.perf_counter() - t0
+    events = sum(n for n, _ in out)
+    per_core = events / sum(dt for _, dt in out)
+    return {"value": events / wall, "unit": "events/s", "cores": threads,
+            "per_core": per_core,
+            "sample": f"{len(jobs)} C3 traces ({events} requests), "
+                      "peakmem.allocator.replay from baseline/_ref, one process per trace"}
 
 
 if __name__ == "__main__":
