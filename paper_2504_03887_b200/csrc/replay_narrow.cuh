@@ -31,6 +31,25 @@
 // 32-bucket register directory or the CTA pool stops with PM_POOL_OVERFLOW
 // and is replayed by the narrow memory-directory tiers below.  Results are
 // bit-identical whichever tier finishes a trace.
+//
+// Per warp (one trace at a time):
+//  * requests arrive 32 at a time by 1-D TMA bulk copy (cp.async.bulk +
+//    mbarrier) into a shared double buffer, one chunk ahead; 8-byte wire
+//    words (pm_replay_host_wire) are decoded there in place;
+//  * each lane gathers its request's handle record; a per-trace handle
+//    watermark says which records belong to this run (no table zeroing);
+//    in-chunk reuse of a handle is forwarded with a ballot, and link
+//    updates to a staged handle are mirrored into the staging copy;
+//  * free blocks live in buckets of <= 32 entries with per-bucket occupancy
+//    masks (a removal clears a bit; entries move only on split / merge),
+//    indexed by a sorted directory in registers (lane d = position d: one
+//    ballot finds a bucket) or, in the retry passes, in shared memory with
+//    a register summary;
+//  * the main pass's warps (24 per SM) share one shared-memory bucket pool
+//    and wait for buckets when it runs dry (one victim per deadlocked CTA
+//    escalates); config constants, peaks and counters that the allocation
+//    path touches live in a per-warp shared record, keeping the kernel at 80
+//    registers.
 #pragma once
 
 #include "replay_device.cuh"
