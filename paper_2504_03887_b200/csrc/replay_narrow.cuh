@@ -194,6 +194,8 @@ struct NDir {
           const unsigned old = atomicOr(&cta_used[w], 1u << b);
           if (!(old & (1u << b))) {
             p = w * 32 + b;
+            // acquire: the previous owner's accesses to the bucket precede ours
+            __threadfence_block();
             break;
           }
           v = old | (1u << b);
@@ -232,10 +234,16 @@ struct NDir {
     int* ctr = reinterpret_cast<int*>(cta_used + cta_words);
     if (lane == 0) atomicExch(&ctr[2], 0);
   }
+  // release: this warp's accesses to the bucket precede the next owner's
+  // (the bucket changes hands through the CTA bitmap's atomics)
   __device__ __forceinline__ void free_phys(int p) {
+    __syncwarp();
+    __threadfence_block();
     if (lane == 0) atomicAnd(&cta_used[p >> 5], ~(1u << (p & 31)));
   }
   __device__ __forceinline__ void release_all() {
+    __syncwarp();
+    __threadfence_block();
     if (lane < nb) atomicAnd(&cta_used[dp >> 5], ~(1u << (dp & 31)));
     nb = 0;
   }
@@ -563,8 +571,9 @@ __device__ __forceinline__ void make_room(const NPool& P, D& dir, NCtx& c,
     const long long sz = (long long)hi(P.ka[id]) << s;
     pool_remove(dir, c, id);
     c.reserved -= sz;
+    const int ns = ws->nseg - 1;  // every lane reads before any lane writes
     __syncwarp();
-    ws->nseg -= 1;  // uniform store
+    ws->nseg = ns;  // uniform store
     __syncwarp();
   }
 }
