@@ -222,6 +222,7 @@ struct DirReg {
           const unsigned old = atomicOr(&cta_used[w], 1u << b);
           if (!(old & (1u << b))) {
             p = w * 32 + b;
+            __threadfence_block();  // acquire the bucket from its last owner
             break;
           }
           v = old | (1u << b);
@@ -231,11 +232,16 @@ struct DirReg {
     }
     return __shfl_sync(kFull, p, 0);
   }
+  // release: this warp's accesses precede the next owner's
   __device__ __forceinline__ void free_phys(int p) {
+    __syncwarp();
+    __threadfence_block();
     if (lane == 0) atomicAnd(&cta_used[p >> 5], ~(1u << (p & 31)));
   }
   // hand every bucket of this warp back to the CTA pool
   __device__ __forceinline__ void release_all() {
+    __syncwarp();
+    __threadfence_block();
     if (lane < nb) atomicAnd(&cta_used[dp >> 5], ~(1u << (dp & 31)));
     nb = 0;
   }
