@@ -346,13 +346,17 @@ int replay_batch_impl(const pm_req_t* reqs, const int64_t* trace_offsets,
     const long long g = atoll(cap);
     if (g > 0 && g < grid) grid = g;
   }
+  // long traces skip to pass 2 only when the batch cannot fill the main
+  // pass (one trace per SM or fewer): otherwise they share the main pass's
+  // throughput like any other trace
+  const int long_trace = n_traces <= occ.sms ? pmn::kLongTrace : pmn::kNoSkip;
 #define PM_LAUNCH_NARROW(W)                                                   \
   pmn::replay_narrow_kernel<W><<<(unsigned)grid, W * 32, occ.smem_n, stream>>>( \
       reqs, trace_offsets, cfgs, cfg_of_trace, results, timeline,             \
       reinterpret_cast<pmb::u32*>(recs), ctl, trace_order, n_traces, list_m1, \
       occ.buckets_n, group_end, n_groups, ready,                             \
       reinterpret_cast<const pmb::u64*>(wire), const_cast<pm_req_t*>(reqs),   \
-      list_w1)
+      list_w1, long_trace)
 #define PM_LAUNCH_MAIN(W)                                                     \
   pmb::replay_smem_kernel<W><<<(unsigned)grid, W * 32, occ.smem, stream>>>(  \
       reqs, trace_offsets, cfgs, cfg_of_trace, results, timeline, recs, ctl, \
@@ -389,18 +393,22 @@ int replay_batch_impl(const pm_req_t* reqs, const int64_t* trace_offsets,
       reqs, trace_offsets, cfgs, cfg_of_trace, results, timeline,
       reinterpret_cast<pmb::u32*>(recs), ctl, pmn::kTierMemSmem, list_m1, list_m2,
       list_w1, nullptr, occ.nbmax_m1, reinterpret_cast<const pmb::u64*>(wire),
-      const_cast<pm_req_t*>(reqs));
+      const_cast<pm_req_t*>(reqs), long_trace);
   e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "replay pass-1 launch");
   {
     const int nbm2 = occ.nbmax_m2 < L.nbmax_g ? occ.nbmax_m2 : L.nbmax_g;
-    const long long gm2 = L.retry_warps < occ.sms ? L.retry_warps : occ.sms;
+    // up to one CTA per SM, as many as the retry region holds
+    long long gm2 = (long long)((L.recs - L.gpool) / pmn::mem_tier_pool_bytes(nbm2));
+    if (gm2 > occ.sms) gm2 = occ.sms;
+    if (gm2 > n_traces) gm2 = n_traces;
+    if (gm2 < 1) gm2 = 1;
     pmn::replay_narrow_mem_kernel<false>
         <<<(unsigned)gm2, 32, pmn::mem_tier_smem(nbm2, false), stream>>>(
             reqs, trace_offsets, cfgs, cfg_of_trace, results, timeline,
             reinterpret_cast<pmb::u32*>(recs), ctl, pmn::kTierMemHbm, list_m2,
             list_w4, list_w1, gpool, nbm2, reinterpret_cast<const pmb::u64*>(wire),
-            const_cast<pm_req_t*>(reqs));
+            const_cast<pm_req_t*>(reqs), pmn::kNoSkip);
     e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "replay pass-2 launch");
   }

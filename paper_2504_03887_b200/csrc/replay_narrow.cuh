@@ -1082,7 +1082,10 @@ __device__ __forceinline__ NStage carve_stage(char* wst) {
 //   3..6 the wide tiers 1-4 of replay_device.cuh            (kTierWide1..)
 // A capacity overflow moves a trace to the next capacity tier; an encoding
 // limit sends it to the first wide tier.
-constexpr int kLongTrace = 1 << 20;  // requests: straight to pass 2
+// requests: a trace this long goes straight to pass 2 when the batch is too
+// small to fill the main pass anyway (the host passes kNoSkip otherwise)
+constexpr int kLongTrace = 1 << 20;
+constexpr int kNoSkip = 0x7FFFFFFF;
 constexpr int kTierMemSmem = 1;
 constexpr int kTierMemHbm = 2;
 constexpr int kTierWide1 = 3;
@@ -1287,7 +1290,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
                          int n_groups, const volatile unsigned* ready,
                          const u64* __restrict__ wire,
                          pm_req_t* __restrict__ expand,
-                         int32_t* __restrict__ enc_list) {
+                         int32_t* __restrict__ enc_list, int long_trace) {
   extern __shared__ __align__(16) char smem[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
@@ -1327,7 +1330,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
     const int tr = list ? list[t] : (int)t;
     if (lane == 0) atomicAdd(active, 1);
     replay_trace(tr, reqs, offs, cfgs, cfg_of, results, timeline, recs, P, dir,
-                 sg, lane, wire, expand, false, kLongTrace);
+                 sg, lane, wire, expand, false, long_trace);
     __syncwarp();
     if (lane == 0) atomicSub(active, 1);
     const int sts = results[tr].status;
@@ -1354,7 +1357,7 @@ __global__ void __launch_bounds__(32, 1)
                              int32_t* __restrict__ enc_list,
                              char* __restrict__ gpool, int nbmax,
                              const u64* __restrict__ wire,
-                             pm_req_t* __restrict__ expand) {
+                             pm_req_t* __restrict__ expand, int long_trace) {
   extern __shared__ __align__(16) char smem[];
   const int lane = threadIdx.x & 31;
   NStage sg = carve_stage(smem);
@@ -1387,7 +1390,7 @@ __global__ void __launch_bounds__(32, 1)
     // the last narrow tier expands wire words for the wide tier it hands to
     replay_trace(tr, reqs, offs, cfgs, cfg_of, results, timeline, recs, P, dir,
                  sg, lane, wire, expand, !SMEM_POOL,
-                 SMEM_POOL ? kLongTrace : 0x7FFFFFFF);
+                 SMEM_POOL ? long_trace : kNoSkip);
     __syncwarp();
     if (lane == 0)
       route(ctl, results[tr].status, tr, SMEM_POOL ? kTierMemHbm : kTierWide4,
