@@ -816,11 +816,20 @@ __global__ void k_order_keys(const RawReq* raw, long long n, long long vmin,
   idx[i] = i;
 }
 
+// min / max virtual timestamp: a warp reduction, then one atomic pair per
+// warp (one pair per element serialised on two addresses)
 __global__ void k_minmax_vts(const RawReq* raw, long long n, long long* mm) {
-  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  atomicMin(&mm[0], raw[i].vts);
-  atomicMax(&mm[1], raw[i].vts);
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  long long lo = INT64_MAX, hi = INT64_MIN;
+  if (i < n) lo = hi = raw[i].vts;
+  for (int o = 16; o > 0; o >>= 1) {
+    lo = min(lo, __shfl_down_sync(0xffffffffu, lo, o));
+    hi = max(hi, __shfl_down_sync(0xffffffffu, hi, o));
+  }
+  if ((threadIdx.x & 31) == 0 && lo <= hi) {
+    atomicMin(&mm[0], lo);
+    atomicMax(&mm[1], hi);
+  }
 }
 
 // packed replay records: handle = raw index of the block's alloc
