@@ -1109,7 +1109,7 @@ __device__ __forceinline__ void route(pmb::Ctl* ctl, int sts, int tr,
 struct NDirMem {
   u64* db;          // [nbmax] bound by position
   int* dp;          // [nbmax] physical bucket by position
-  unsigned* m;      // [nbmax] occupancy mask by physical bucket
+  unsigned* m;      // [nbmax] occupancy mask by position
   int* pos;         // [nbmax] position by physical bucket
   int* pstack;      // [nbmax] free physical buckets
   int nb, ptop, nbmax, lane;
@@ -1155,11 +1155,10 @@ struct NDirMem {
     return b ? lo_ + 31 - __clz(b) : lo_;
   }
   __device__ __forceinline__ int phys(int d) const { return dp[d]; }
-  __device__ __forceinline__ unsigned mask(int d) const { return m[dp[d]]; }
+  __device__ __forceinline__ unsigned mask(int d) const { return m[d]; }
   __device__ __forceinline__ void set_mask(int d, unsigned v) {
-    const int p = dp[d];
     __syncwarp();
-    m[p] = v;  // uniform store
+    m[d] = v;  // uniform store
     __syncwarp();
   }
   __device__ __forceinline__ void set_bit(int d, int b) {
@@ -1173,7 +1172,7 @@ struct NDirMem {
     for (int base = 0; base < nb - 1; base += 32) {
       const int x = base + lane;
       bool ok = false;
-      if (x < nb - 1) ok = __popc(m[dp[x]]) + __popc(m[dp[x + 1]]) <= kBucket;
+      if (x < nb - 1) ok = __popc(m[x]) + __popc(m[x + 1]) <= kBucket;
       const unsigned b = __ballot_sync(kFull, ok);
       if (b) return base + __ffs(b) - 1;
     }
@@ -1186,21 +1185,24 @@ struct NDirMem {
       const bool mv = e < nb;
       u64 xb = 0;
       int xp = 0;
+      unsigned xm = 0;
       if (mv) {
         xb = db[e];
         xp = dp[e];
+        xm = m[e];
       }
       __syncwarp();
       if (mv) {
         db[e + 1] = xb;
         dp[e + 1] = xp;
+        m[e + 1] = xm;
         pos[xp] = e + 1;
       }
       __syncwarp();
     }
     db[d] = b;
     dp[d] = p;
-    m[p] = mk;
+    m[d] = mk;
     pos[p] = d;
     __syncwarp();
     nb += 1;
@@ -1212,14 +1214,17 @@ struct NDirMem {
       const bool mv = e < nb;
       u64 xb = 0;
       int xp = 0;
+      unsigned xm = 0;
       if (mv) {
         xb = db[e];
         xp = dp[e];
+        xm = m[e];
       }
       __syncwarp();
       if (mv) {
         db[e - 1] = xb;
         dp[e - 1] = xp;
+        m[e - 1] = xm;
         pos[xp] = e - 1;
       }
       __syncwarp();
