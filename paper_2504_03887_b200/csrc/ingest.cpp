@@ -19,6 +19,7 @@
 // streamed from the columns -- ensure_ascii escaping included.
 
 #include <algorithm>
+#include <atomic>
 #include <cerrno>
 #include <charconv>
 #include <cmath>
@@ -914,27 +915,21 @@ int pm_bundle_digest(int64_t n, const int8_t* cat, const int64_t* start,
     size_t max_name = 0;
     for (const std::string& x : esc) max_name = std::max(max_name, x.size());
     const size_t max_event = 512 + max_name;
-    std::vector<char> buf(std::max<size_t>(1 << 17, 2 * max_event));
-    size_t pos = 0;
-    char* const B = buf.data();
-    auto put = [&](const char* p, size_t m) {
-      memcpy(B + pos, p, m);
-      pos += m;
-    };
-    auto num = [&](int64_t v) {
-      pos = (size_t)(std::to_chars(B + pos, B + pos + 24, v).ptr - B);
-    };
     static const char kArgs[] = "{\"args\":{";
     static const char kCat[] = "},\"cat\":\"";
     static const char kDur[] = "\",\"dur\":";
     static const char kName[] = ",\"name\":";
     static const char kPhI[] = ",\"ph\":\"i\",\"ts\":";
     static const char kPhX[] = ",\"ph\":\"X\",\"ts\":";
-    for (int64_t e = 0; e < n; ++e) {
-      if (pos + max_event > buf.size()) {
-        o.sh.update(B, pos);
-        pos = 0;
-      }
+    // one event at B + pos (room for max_event bytes guaranteed)
+    auto emit = [&](char* B, size_t& pos, int64_t e) {
+      auto put = [&](const char* p, size_t m) {
+        memcpy(B + pos, p, m);
+        pos += m;
+      };
+      auto num = [&](int64_t v) {
+        pos = (size_t)(std::to_chars(B + pos, B + pos + 24, v).ptr - B);
+      };
       if (e) B[pos++] = ',';
       put(kArgs, sizeof kArgs - 1);
       bool first = true;
@@ -960,8 +955,63 @@ int pm_bundle_digest(int64_t n, const int8_t* cat, const int64_t* start,
         put(kPhX, sizeof kPhX - 1);
       num(start[e]);
       B[pos++] = '}';
+    };
+    const size_t cap = std::max<size_t>(1 << 18, 2 * max_event);
+    if (n < 20000 || std::thread::hardware_concurrency() < 2) {
+      std::vector<char> buf(cap);
+      size_t pos = 0;
+      for (int64_t e = 0; e < n; ++e) {
+        if (pos + max_event > cap) {
+          o.sh.update(buf.data(), pos);
+          pos = 0;
+        }
+        emit(buf.data(), pos, e);
+      }
+      o.sh.update(buf.data(), pos);
+    } else {
+      // a formatter thread fills a ring of buffers while this thread hashes
+      // them in order: formatting and SHA-256 overlap
+      constexpr int K = 4;
+      std::vector<std::vector<char>> ring(K, std::vector<char>(cap));
+      std::atomic<int> ready[K];
+      size_t len[K];
+      for (int k = 0; k < K; ++k) ready[k].store(0);
+      std::atomic<int64_t> sealed{-1};  // total buffers, once known
+      std::thread fmt([&] {
+        int64_t b = 0;
+        size_t pos = 0;
+        auto seal = [&] {
+          const int slot = (int)(b % K);
+          len[slot] = pos;
+          ready[slot].store(1, std::memory_order_release);
+          ++b;
+          pos = 0;
+          const int next = (int)(b % K);
+          while (ready[next].load(std::memory_order_acquire) != 0)
+            std::this_thread::yield();
+        };
+        for (int64_t e = 0; e < n; ++e) {
+          if (pos + max_event > cap) seal();
+          emit(ring[b % K].data(), pos, e);
+        }
+        seal();
+        sealed.store(b, std::memory_order_release);
+      });
+      for (int64_t i = 0;; ++i) {
+        const int slot = (int)(i % K);
+        for (;;) {
+          if (ready[slot].load(std::memory_order_acquire)) break;
+          const int64_t t = sealed.load(std::memory_order_acquire);
+          if (t >= 0 && i >= t) break;
+          std::this_thread::yield();
+        }
+        const int64_t t = sealed.load(std::memory_order_acquire);
+        if (!ready[slot].load(std::memory_order_acquire) && t >= 0 && i >= t) break;
+        o.sh.update(ring[slot].data(), len[slot]);
+        ready[slot].store(0, std::memory_order_release);
+      }
+      fmt.join();
     }
-    o.sh.update(B, pos);
   }
   o.s("]}}");
   o.done(hex_out);
