@@ -151,7 +151,8 @@ int pm_replay_host(const pm_req_t* reqs, const int64_t* trace_offsets,
  * request does not fit (an alloc of another handle, a stream, a size < 1 or
  * >= 2^62, an unknown kind), in which case the caller uses pm_replay_host.
  * pm_replay_host_wire is pm_replay_host on wire words: half the H2D bytes,
- * bit-identical results. */
+ * bit-identical results.  pm_wire_pack runs on host threads (contiguous runs
+ * of traces), so packing keeps up with the zero-copy replay. */
 #define PM_WIRE_FREE (1ull << 62)
 int pm_wire_pack(const pm_req_t* reqs, const int64_t* trace_offsets,
                  int32_t n_traces, uint64_t* words, int64_t* first_bad);

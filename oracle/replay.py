@@ -50,6 +50,8 @@ def load():
         lib.oracle_replay_batch.restype = ctypes.c_int
         lib.oracle_replay_batch.argtypes = [vp, vp, ctypes.c_int32, vp, vp, vp,
                                             vp, ctypes.c_int32]
+        lib.pm_synth_counts_ids.argtypes = [vp, ctypes.c_int32, vp, ctypes.c_int]
+        lib.pm_synth_fill_ids.argtypes = [vp, ctypes.c_int32, vp, vp, ctypes.c_int]
         _lib = lib
     return _lib
 
@@ -76,3 +78,20 @@ def replay_batch(reqs: np.ndarray, offsets: np.ndarray, cfgs: np.ndarray,
     lib.oracle_replay_batch(_p(reqs), _p(offsets), n, _p(cfgs), _p(cfg_of),
                             _p(res), _p(tl), int(n_threads))
     return res, tl
+
+
+def c3_traces(ids, n_threads: int | None = None):
+    """(reqs, offsets) of C3 traces `ids` from the generator compiled into
+    this library (workloads/c3gen.c == oracle/c3gen.py), so the reference
+    bench arm needs no engine library."""
+    lib = load()
+    ids = np.ascontiguousarray(ids, dtype=np.int32)
+    if n_threads is None:
+        n_threads = len(os.sched_getaffinity(0))
+    counts = np.zeros(len(ids), dtype=np.int64)
+    lib.pm_synth_counts_ids(_p(ids), len(ids), _p(counts), int(n_threads))
+    offs = np.zeros(len(ids) + 1, dtype=np.int64)
+    np.cumsum(counts, out=offs[1:])
+    reqs = np.empty(int(offs[-1]), dtype=REQ_DTYPE)
+    lib.pm_synth_fill_ids(_p(ids), len(ids), _p(offs), _p(reqs), int(n_threads))
+    return reqs, offs

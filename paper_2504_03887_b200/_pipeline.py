@@ -10,7 +10,7 @@ import numpy as np
 
 from . import _native
 from ._native import LIB_DIR, REQ_DTYPE
-from .errors import EngineUnavailable
+from .errors import EngineLimitExceeded, EngineUnavailable
 
 LIB_PATH = LIB_DIR / "libpeakmem_pipeline.so"
 EXPORTED_SYMBOLS = ("pm_pipeline_last_error", "pm_sort_events", "pm_link",
@@ -103,12 +103,23 @@ def layer_tree(pid, par, is_layer, start, event_id=None):
     return node_parent[:nl], child_order[:nl], child_off, walk[:n_walk.value]
 
 
+def _check_seq_range(seq, n_ops: int) -> None:
+    """The sequence-number join sorts (root << 32 | seq) keys
+    (csrc/pipeline.cu k_seq_keys): sequence numbers and root ids must fit in
+    32 bits.  The reference keeps unbounded ints, so larger values are an
+    engine limit, never a silent truncation."""
+    if n_ops >= 1 << 32 or (len(seq) and int(seq.max()) >= 1 << 32):
+        raise EngineLimitExceeded(
+            "sequence numbers and operator counts must be below 2^32")
+
+
 class LinkResult:
     """Columnar output of pm_link (see csrc/pipeline.cu)."""
 
 
 def link(op_start, op_end, op_seq, in_start, in_addr, in_nbytes,
          l_start, l_end) -> LinkResult:
+    _check_seq_range(_i64(op_seq), len(op_start))
     lib = load()
     _native.require_device()
     op_start, op_end, op_seq = map(_i64, (op_start, op_end, op_seq))
@@ -169,6 +180,7 @@ def link(op_start, op_end, op_seq, in_start, in_addr, in_nbytes,
 def link_roots(root_start, root_end, root_seq_off, root_seq, l_start, l_end,
                b_alloc, b_free) -> LinkResult:
     """The join on GIVEN roots (linking.py:126-132 with any root set)."""
+    _check_seq_range(_i64(root_seq), len(root_start))
     lib = load()
     _native.require_device()
     root_start, root_end, root_seq_off, root_seq = map(

@@ -22,6 +22,8 @@ replay runs in the CUDA kernel -- there is no CPU replay path here.
 
 from __future__ import annotations
 
+import math
+
 import json
 from dataclasses import dataclass, field
 from typing import Iterable, Sequence
@@ -139,6 +141,23 @@ class PackedTrace:
     kinds_raw: dict[int, object]
 
 
+def _int_size(size):
+    """The integer the engine replays for a request size, or None.
+
+    round_request (allocator.py:79-83) only compares and ceil-divides the
+    size, so a finite float replays like ceil(size): ceil(x / a) ==
+    ceil(ceil(x) / a) for an integer alignment a, and size <= 0 iff
+    ceil(size) <= 0.  (The reference's timeline then holds floats of the same
+    values.)"""
+    if isinstance(size, (int, np.integer)) and not isinstance(size, bool):
+        return int(size)
+    if isinstance(size, (float, np.floating)) and math.isfinite(size):
+        return int(math.ceil(size))
+    if isinstance(size, bool):
+        return int(size)
+    return None
+
+
 def pack_trace(requests: Iterable[dict]) -> PackedTrace:
     """Intern block ids and streams into dense per-trace integers.
 
@@ -168,12 +187,19 @@ def pack_trace(requests: Iterable[dict]) -> PackedTrace:
                 bid = req["block_id"]
                 size = req["size"]
                 stream = req.get("stream", 0)
+                seen = bid in handle_ids
                 h = handle_ids.setdefault(bid, len(handle_ids))
                 sid = stream_ids.setdefault(stream, len(stream_ids))
-                size = int(size) if isinstance(size, (int, np.integer)) else size
-                if not isinstance(size, int):
-                    raise TypeError(
-                        f"the B200 engine needs integer sizes, got {size!r}")
+                size = _int_size(size)
+                if size is None:
+                    if seen:
+                        # allocate() checks the handle first (allocator.py:
+                        # 274-276): a reused handle is DuplicateHandle whatever
+                        # its size -- any positive size lets the kernel say so
+                        size = 1
+                    else:
+                        raise TypeError(
+                            f"'<=' not supported for size {req['size']!r}")
                 if size > _INT64_MAX:
                     size = 1 << 62  # replays as PM_SIZE_LIMIT
                 elif size < -_INT64_MAX:

@@ -17,6 +17,7 @@
 #include <cstdlib>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 namespace {
@@ -769,24 +770,53 @@ int pm_wire_pack(const pm_req_t* reqs, const int64_t* trace_offsets,
   if (first_bad) *first_bad = -1;
   if (n_traces < 0 || (n_traces > 0 && (!trace_offsets || !words)))
     return fail(PM_ERR_INVALID_ARGUMENT, "pm_wire_pack: bad arguments");
-  for (int32_t t = 0; t < n_traces; ++t) {
-    int64_t allocs = 0;
-    for (int64_t i = trace_offsets[t]; i < trace_offsets[t + 1]; ++i) {
-      const pm_req_t& r = reqs[i];
-      const uint32_t kind = r.kind_stream & 3u;
-      if (kind == PM_KIND_ALLOC && (r.kind_stream >> 2) == 0 &&
-          r.handle == allocs && r.size >= 1 && r.size < (int64_t)(1ll << 62)) {
-        words[i] = (uint64_t)r.size;
-        ++allocs;
-      } else if (kind == PM_KIND_FREE && r.handle >= 0) {
-        words[i] = PM_WIRE_FREE | (uint64_t)(uint32_t)r.handle;
-      } else {
-        if (first_bad) *first_bad = i;
-        return fail(PM_ERR_INVALID_ARGUMENT,
-                    "pm_wire_pack: request " + std::to_string(i) +
-                        " has no wire encoding");
+  if (n_traces == 0) return PM_SUCCESS;
+  // Traces are independent (each numbers its own handles), so host threads
+  // pack contiguous runs of traces of ~equal request counts; the lowest bad
+  // index over all threads is the one reported.
+  const int64_t total = trace_offsets[n_traces] - trace_offsets[0];
+  unsigned hw = std::thread::hardware_concurrency();
+  int nt = (int)std::min<int64_t>(hw ? hw : 1, std::max<int64_t>(1, total >> 20));
+  nt = std::min(nt, (int)n_traces);
+  std::vector<int64_t> bad(nt, INT64_MAX);
+  auto work = [&](int w) {
+    // traces [t0, t1) of worker w: split by cumulative request count
+    auto cut = [&](int k) -> int32_t {
+      const int64_t target = trace_offsets[0] + total * k / nt;
+      return (int32_t)(std::lower_bound(trace_offsets, trace_offsets + n_traces, target) -
+                       trace_offsets);
+    };
+    const int32_t t0 = w == 0 ? 0 : cut(w), t1 = w == nt - 1 ? n_traces : cut(w + 1);
+    for (int32_t t = t0; t < t1; ++t) {
+      int64_t allocs = 0;
+      for (int64_t i = trace_offsets[t]; i < trace_offsets[t + 1]; ++i) {
+        const pm_req_t& r = reqs[i];
+        const uint32_t kind = r.kind_stream & 3u;
+        if (kind == PM_KIND_ALLOC && (r.kind_stream >> 2) == 0 &&
+            r.handle == allocs && r.size >= 1 && r.size < (int64_t)(1ll << 62)) {
+          words[i] = (uint64_t)r.size;
+          ++allocs;
+        } else if (kind == PM_KIND_FREE && r.handle >= 0) {
+          words[i] = PM_WIRE_FREE | (uint64_t)(uint32_t)r.handle;
+        } else {
+          bad[w] = i;
+          return;
+        }
       }
     }
+  };
+  if (nt == 1) {
+    work(0);
+  } else {
+    std::vector<std::thread> th;
+    for (int w = 0; w < nt; ++w) th.emplace_back(work, w);
+    for (auto& x : th) x.join();
+  }
+  const int64_t b = *std::min_element(bad.begin(), bad.end());
+  if (b != INT64_MAX) {
+    if (first_bad) *first_bad = b;
+    return fail(PM_ERR_INVALID_ARGUMENT,
+                "pm_wire_pack: request " + std::to_string(b) + " has no wire encoding");
   }
   return PM_SUCCESS;
 }

@@ -20,6 +20,7 @@ from __future__ import annotations
 
 import functools
 import importlib
+import sys
 
 from . import errors as _our_errors
 from .allocator import replay as _gpu_replay
@@ -78,13 +79,17 @@ def install(pipeline: bool = False, module: str = "peakmem") -> None:
     if pipeline:
         from . import orchestration as ours
         ref_orch = importlib.import_module(f"{module}.orchestration")
+        ref_analysis = importlib.import_module(f"{module}.analysis")
+        ref_build = _original(ref_orch, "build_sequence")
 
         def analyze(bundle):
             return ours.analyze(_ref_bundle(bundle))
 
-        ref_analysis = importlib.import_module(f"{module}.analysis")
-
         def build_sequence(analyzed, iterations=2):
+            if not isinstance(analyzed, ours.AnalyzedTrace):
+                # an AnalyzedTrace the reference built itself (e.g. before
+                # install()): its own enums and objects, its own function
+                return ref_build(analyzed, iterations)
             seq = ours.build_sequence(analyzed, iterations)
             kinds = {"alloc": ref_orch.RequestKind.ALLOC,
                      "free": ref_orch.RequestKind.FREE}
@@ -98,14 +103,27 @@ def install(pipeline: bool = False, module: str = "peakmem") -> None:
                 requests=reqs, iteration_boundaries=seq.iteration_boundaries,
                 phase_tags=tags)
 
-        targets += [(ref_est, "analyze", _translate(analyze, ref_errors)),
-                    (ref_est, "build_sequence",
-                     _translate(build_sequence, ref_errors)),
-                    (ref_orch, "analyze", _translate(analyze, ref_errors))]
+        # every alias of the pair moves together (estimator.py:12-17 binds
+        # them at import, __init__.py:71 re-exports them), so the reference's
+        # own build_sequence never sees the engine's AnalyzedTrace
+        gpu_analyze = _translate(analyze, ref_errors)
+        gpu_build = _translate(build_sequence, ref_errors)
+        for mod in (ref_est, ref_orch, ref):
+            targets += [(mod, "analyze", gpu_analyze),
+                        (mod, "build_sequence", gpu_build)]
+    cli = sys.modules.get(f"{module}.cli")
+    if cli is not None:  # cli.py:24 binds replay at import (used at :188)
+        targets.append((cli, "replay", gpu_replay))
     for mod, name, fn in targets:
         key = (mod.__name__, name)
         _saved.setdefault(key, (mod, getattr(mod, name)))
         setattr(mod, name, fn)
+
+
+def _original(mod, name):
+    """The reference's own function, even if install() already ran."""
+    saved = _saved.get((mod.__name__, name))
+    return saved[1] if saved else getattr(mod, name)
 
 
 def uninstall() -> None:

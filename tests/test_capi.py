@@ -176,3 +176,27 @@ def test_wire_pack_roundtrip_and_rejections():
                 [{"seq_no": 0, "kind": "resize", "block_id": "a", "size": 5}]):
         q = pack_trace(bad)
         assert _native.wire_pack(q.reqs, np.array([0, len(q.reqs)])) is None
+
+
+def test_wire_pack_threaded_matches_scalar_rule():
+    """pm_wire_pack splits traces over host threads: on a multi-million
+    request batch every word follows the single-trace rule, and the LOWEST
+    bad index is reported whichever thread finds it."""
+    from paper_2504_03887_b200 import synth
+    reqs, offs = synth.generate(40, first=123)
+    w = _native.wire_pack(reqs, offs)
+    alloc = (reqs["kind_stream"] & 3) == 0
+    assert (w[alloc] == reqs["size"][alloc].astype(np.uint64)).all()
+    want_free = np.uint64(1 << 62) | reqs["handle"][~alloc].astype(np.uint64)
+    assert (w[~alloc] == want_free).all()
+    bad = reqs.copy()
+    late, early = int(offs[35]) + 7, int(offs[20]) + 3
+    bad["kind_stream"][late] = 2
+    bad["kind_stream"][early] = 2
+    lib = _native.load_library()
+    import ctypes
+    out = np.empty(len(bad), np.uint64)
+    first = ctypes.c_int64(-1)
+    rc = lib.pm_wire_pack(_native._p(bad), _native._p(offs), len(offs) - 1,
+                          _native._p(out), ctypes.byref(first))
+    assert rc != 0 and first.value == early
