@@ -772,7 +772,15 @@ __device__ __forceinline__ void replay_trace(
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
     }
-    const int my_h = lane < cnt ? (int)lo(cb[lane].y) : -1;
+    // Chunk prologue, lane-parallel (lane i = request cbase + i): decode the
+    // request once, check everything that does not depend on the replay
+    // state (kind, handle range, size, stream, encoding) and round the size,
+    // find the latest earlier request of the chunk on the same handle (its
+    // staged record is the one this request reads), and gather the handle's
+    // record.  The serial loop below then reads one packed 16 B word per
+    // request.
+    const ulonglong2 evl = lane < cnt ? cb[lane] : make_ulonglong2(0ull, 0ull);
+    const int my_h = lane < cnt ? (int)lo(evl.y) : -1;
     const bool hok = my_h >= 0 && my_h < n;
     const bool fresh = hok && my_h > wm;
     {
@@ -792,33 +800,62 @@ __device__ __forceinline__ void replay_trace(
       }
     }
     uint4 r = make_uint4(0, 0, 0, 0);
-    if (hok && !fresh) r = *rec.rec((u32)my_h);
+    uint4* const myrec = rec.rec((u32)(hok ? my_h : 0));
+    if (hok && !fresh) r = *myrec;
     uint4* st = sg.rec;
     st[lane] = r;
     const int hcmp = hok ? my_h : -1;
+    {
+      const unsigned kind_l = hi(evl.y) & 3u;
+      int pre = PM_OK;
+      u32 ru_l = 0;
+      if (kind_l >= PM_KIND_UNKNOWN) {
+        pre = kind_l == PM_KIND_UNKNOWN ? PM_UNKNOWN_KIND : PM_MISSING_FIELD;
+      } else if (!hok) {
+        pre = PM_BAD_HANDLE;
+      } else if (kind_l == PM_KIND_ALLOC) {
+        // checked after the duplicate-handle test at replay time
+        const long long size = (long long)evl.x;
+        const uint4 kc = *reinterpret_cast<const uint4*>(ws);  // amask, lim
+        const u64 rounded = (((u64)size + kc.x) & ~(u64)kc.x) >> s;
+        if (size <= 0)
+          pre = PM_ZERO_SIZE;
+        else if ((hi(evl.y) >> 2) != 0u || rounded > (u64)kc.y)
+          pre = PM_ENCODING_LIMIT;  // outside the encoding: wide tiers
+        else
+          ru_l = (u32)rounded;
+      }
+      const unsigned same = __match_any_sync(kFull, hcmp);
+      const unsigned earlier = same & lanemask_lt();
+      const int src_l = earlier ? 31 - __clz(earlier) : lane;
+      __syncwarp();
+      // x ru, y handle, z kind | pre << 2 | src << 8
+      if (lane < cnt)
+        reinterpret_cast<uint4*>(cb)[lane] = make_uint4(
+            ru_l, (u32)my_h, kind_l | ((u32)pre << 2) | ((u32)src_l << 8), 0u);
+      // generic writes into a TMA destination precede its async refill
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
     __syncwarp();
 
-    ulonglong2 ev_next = cb[0];
+    uint4 ev_next = reinterpret_cast<const uint4*>(cb)[0];
     for (int j = 0; j < cnt; ++j) {
-      // the next request's load is issued before this one's dependent chain
-      const ulonglong2 ev = ev_next;
-      if (j + 1 < cnt) ev_next = cb[j + 1];
-      const long long size = (long long)ev.x;
-      const int hj = (int)lo(ev.y);
-      const unsigned ks = hi(ev.y);
-      const unsigned kind = ks & 3u;
-      const unsigned m = __ballot_sync(kFull, hcmp == hj) & ((1u << j) - 1u);
-      const int src = m ? 31 - __clz(m) : j;
+      // the next request's word is loaded before this one's dependent chain
+      // (slot 32 lies inside the staging area: read, never used)
+      const uint4 ev = ev_next;
+      ev_next = reinterpret_cast<const uint4*>(cb)[j + 1];
+      const int hj = (int)ev.y;
+      const unsigned kind = ev.z & 3u;
+      const int pre = (int)((ev.z >> 2) & 63u);
+      const int src = (int)(ev.z >> 8);
       int sts = PM_OK;
-      if (kind >= PM_KIND_UNKNOWN) {
-        sts = kind == PM_KIND_UNKNOWN ? PM_UNKNOWN_KIND : PM_MISSING_FIELD;
-      } else if ((unsigned)hj >= (unsigned)n) {
-        sts = PM_BAD_HANDLE;
+      if (kind >= PM_KIND_UNKNOWN || pre == PM_BAD_HANDLE) {
+        sts = pre;
       } else {
         const uint4 rj = st[src];
         // the allocation constants, loaded alongside the record
         const uint4 kc = *reinterpret_cast<const uint4*>(ws);
-        const u32 k_amask = kc.x, k_lim = kc.y, k_span = kc.z, k_split = kc.w;
+        const u32 k_span = kc.z, k_split = kc.w;
         int rm_id = -1;
         bool up = false;
         int up_id = -1;
@@ -835,13 +872,10 @@ __device__ __forceinline__ void replay_trace(
         if (is_alloc) {
           if (rj.y != 0) {
             sts = PM_DUPLICATE_HANDLE;
-          } else if (size <= 0) {
-            sts = PM_ZERO_SIZE;
-          } else if ((ks >> 2) != 0u ||
-                     ((((u64)size + k_amask) & ~(u64)k_amask) >> s) > (u64)k_lim) {
-            sts = PM_ENCODING_LIMIT;  // outside the encoding: wide tiers
+          } else if (pre != PM_OK) {
+            sts = pre;  // zero size / outside the encoding
           } else {
-            const u32 ru = (u32)((((u64)size + k_amask) & ~(u64)k_amask) >> s);
+            const u32 ru = ev.x;
             const u32 split_lim = k_split;
             u64 KA = 0, Lk = 0;
             const int id = best_fit(P, dir, ru, k_span, lane, KA, Lk);
@@ -984,11 +1018,11 @@ __device__ __forceinline__ void replay_trace(
             if (lane == j) {
               const uint4 o = make_uint4(out_a, out_s, out_L, out_R);
               st[j] = o;
-              *rec.rec((u32)hj) = o;
+              *myrec = o;
             }
           } else if (lane == j) {
             st[j].y = kFreedU;
-            *rec.word((u32)hj, 1) = kFreedU;
+            reinterpret_cast<u32*>(myrec)[1] = kFreedU;
           }
         }
       }
