@@ -77,9 +77,37 @@ typedef enum {
   PM_SIZE_LIMIT = 9,       /* a block >= 2^46 B: outside the engine's range */
   PM_BAD_STREAM = 10,      /* stream id >= 65536                            */
   PM_POOL_OVERFLOW = 11,   /* internal; resolved by the global-pool retry   */
-  PM_ENCODING_LIMIT = 12   /* internal; the narrow pass hands the trace to
+  PM_ENCODING_LIMIT = 12,  /* internal; the narrow pass hands the trace to
                               the wide (64-bit) tiers                       */
+  PM_INVARIANT_VIOLATION = 13 /* validating build only (libpeakmem_b200_
+                              validate.so, -DPM_VALIDATE): the allocator
+                              state broke an invariant of check_invariants
+                              (allocator.py:324-354) after request
+                              stop_index; max_free_blocks holds the
+                              pm_invariant_t code -> AssertionError        */
 } pm_status_t;
+
+/* Invariants the validating build checks after EVERY applied request
+ * (AllocatorState.check_invariants, allocator.py:324-354, run after each
+ * allocate / free when validate=True, :291-292 / :319-320), restated over
+ * the engine's state (free-entry index + per-handle records with neighbour
+ * refs instead of per-segment block chains): */
+typedef enum {
+  PM_INV_BLOCK_SIZE = 1,    /* a block of size <= 0 ("blk.size > 0")         */
+  PM_INV_UNALIGNED = 2,     /* size % alignment != 0 ("unaligned block")     */
+  PM_INV_LINK = 3,          /* a neighbour ref that is not mutual, not live
+                               or not address-contiguous ("tiling gap /
+                               overlap", "broken back-link")               */
+  PM_INV_ADJACENT_FREE = 4, /* two free blocks adjacent ("adjacent free")   */
+  PM_INV_SEGMENTS = 5,      /* chain heads / tails != segments              */
+  PM_INV_CONSERVATION = 6,  /* free + allocated != reserved ("conservation") */
+  PM_INV_ALLOCATED = 7,     /* live blocks != allocated_bytes               */
+  PM_INV_POOL = 8,          /* pool entries != free blocks of the chains, or
+                               an entry outside its index range ("pool and
+                               segment chains disagree")                   */
+  PM_INV_CAPACITY = 9,      /* reserved > device_capacity                   */
+  PM_INV_STREAM = 10        /* neighbours on different streams              */
+} pm_invariant_t;
 
 typedef struct {
   int64_t peak_reserved;
@@ -106,6 +134,13 @@ typedef enum {
 
 const char* pm_last_error(void);
 int pm_version(void);
+
+/* Validating build only (libpeakmem_b200_validate.so): corrupt the state
+ * right after request `request_index` of every trace so tests can see the
+ * invariant checks fire (kind 1: allocated_bytes off by one unit; kind 2: a
+ * neighbour ref that is not mutual; 0: off).  The regular build returns
+ * PM_ERR_INVALID_ARGUMENT. */
+int pm_validate_inject(int64_t request_index, int32_t kind);
 
 /* Bytes of device workspace pm_replay_batch needs for a batch with
  * `total_events` requests, whose longest trace has `max_trace_events`. */

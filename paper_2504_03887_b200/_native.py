@@ -17,6 +17,8 @@ from .errors import EngineUnavailable
 
 LIB_DIR = Path(__file__).resolve().parent / "lib"
 LIB_PATH = LIB_DIR / "libpeakmem_b200.so"
+# the same kernels built with -DPM_VALIDATE: replay(validate=True)
+VALIDATE_LIB_PATH = LIB_DIR / "libpeakmem_b200_validate.so"
 
 # --- packed layouts (must match include/peakmem_b200.h) --------------------
 
@@ -38,15 +40,28 @@ KIND_ALLOC, KIND_FREE, KIND_UNKNOWN, KIND_MISSING = 0, 1, 2, 3
 
 (PM_OK, PM_OOM, PM_UNKNOWN_HANDLE, PM_DOUBLE_FREE, PM_DUPLICATE_HANDLE,
  PM_ZERO_SIZE, PM_UNKNOWN_KIND, PM_MISSING_FIELD, PM_BAD_HANDLE,
- PM_SIZE_LIMIT, PM_BAD_STREAM, PM_POOL_OVERFLOW, PM_ENCODING_LIMIT) = range(13)
+ PM_SIZE_LIMIT, PM_BAD_STREAM, PM_POOL_OVERFLOW, PM_ENCODING_LIMIT,
+ PM_INVARIANT_VIOLATION) = range(14)
+
+#: pm_invariant_t (include/peakmem_b200.h) -> the check_invariants assertion
+#: it restates (allocator.py:324-354)
+INVARIANTS = {1: "blk.size > 0", 2: "unaligned block",
+              3: "tiling gap/overlap or broken back-link",
+              4: "adjacent free blocks", 5: "blocks do not tile segment",
+              6: "conservation", 7: "allocated_total == allocated_bytes",
+              8: "pool and segment chains disagree",
+              9: "reserved_bytes <= device_capacity",
+              10: "neighbouring blocks on different streams"}
 
 #: every symbol include/peakmem_b200.h declares
-EXPORTED_SYMBOLS = ("pm_last_error", "pm_version", "pm_replay_workspace_bytes",
+EXPORTED_SYMBOLS = ("pm_last_error", "pm_version", "pm_validate_inject",
+                    "pm_replay_workspace_bytes",
                     "pm_replay_batch", "pm_replay_host", "pm_wire_pack",
                     "pm_replay_host_wire",
                     "pm_capacity_workspace_bytes", "pm_capacity_search")
 
 _lib = None
+_vlib = None
 
 
 def _p(arr) -> ctypes.c_void_p:
@@ -71,6 +86,8 @@ def load_library(path: Path | str | None = None) -> ctypes.CDLL:
     lib.pm_last_error.argtypes = []
     lib.pm_version.restype = ctypes.c_int
     lib.pm_version.argtypes = []
+    lib.pm_validate_inject.restype = ctypes.c_int
+    lib.pm_validate_inject.argtypes = [i64, i32]
     lib.pm_replay_workspace_bytes.restype = ctypes.c_int
     lib.pm_replay_workspace_bytes.argtypes = [
         i64, i64, i32, ctypes.POINTER(ctypes.c_size_t)]
@@ -93,6 +110,18 @@ def load_library(path: Path | str | None = None) -> ctypes.CDLL:
     if path is None:
         _lib = lib
     return lib
+
+
+def load_validate_library() -> ctypes.CDLL:
+    """The validating build of the engine (same ABI, -DPM_VALIDATE)."""
+    global _vlib
+    if _vlib is None:
+        if not VALIDATE_LIB_PATH.exists():
+            raise EngineUnavailable(
+                f"validating engine library {VALIDATE_LIB_PATH} is not built; "
+                "run __graft_entry__.build()")
+        _vlib = load_library(VALIDATE_LIB_PATH)
+    return _vlib
 
 
 def check(rc: int, lib=None) -> None:
@@ -126,9 +155,9 @@ def workspace_bytes(total_events: int, max_trace_events: int,
 
 def replay_host(reqs: np.ndarray, offsets: np.ndarray, cfgs: np.ndarray,
                 cfg_of: np.ndarray | None, want_timeline: bool,
-                stream: int = 0):
+                stream: int = 0, validate: bool = False):
     """Host-buffer replay through pm_replay_host (H2D + kernel + D2H)."""
-    lib = load_library()
+    lib = load_validate_library() if validate else load_library()
     require_device()
     reqs = np.ascontiguousarray(reqs, dtype=REQ_DTYPE)
     offsets = np.ascontiguousarray(offsets, dtype=np.int64)
@@ -167,9 +196,9 @@ def wire_pack(reqs: np.ndarray, offsets: np.ndarray, out: np.ndarray | None = No
 
 def replay_host_wire(words: np.ndarray, offsets: np.ndarray, cfgs: np.ndarray,
                      cfg_of: np.ndarray | None, want_timeline: bool,
-                     stream: int = 0):
+                     stream: int = 0, validate: bool = False):
     """Host-buffer replay of wire words through pm_replay_host_wire."""
-    lib = load_library()
+    lib = load_validate_library() if validate else load_library()
     require_device()
     words = np.ascontiguousarray(words, dtype=np.uint64)
     offsets = np.ascontiguousarray(offsets, dtype=np.int64)
@@ -188,10 +217,12 @@ def replay_host_wire(words: np.ndarray, offsets: np.ndarray, cfgs: np.ndarray,
 
 def replay_host_auto(reqs: np.ndarray, offsets: np.ndarray, cfgs: np.ndarray,
                      cfg_of: np.ndarray | None, want_timeline: bool,
-                     stream: int = 0):
+                     stream: int = 0, validate: bool = False):
     """pm_replay_host_wire when every request has a wire encoding (half the
     H2D bytes), else pm_replay_host; results are identical."""
     words = wire_pack(reqs, offsets) if len(reqs) else None
     if words is not None:
-        return replay_host_wire(words, offsets, cfgs, cfg_of, want_timeline, stream)
-    return replay_host(reqs, offsets, cfgs, cfg_of, want_timeline, stream)
+        return replay_host_wire(words, offsets, cfgs, cfg_of, want_timeline,
+                                stream, validate)
+    return replay_host(reqs, offsets, cfgs, cfg_of, want_timeline, stream,
+                       validate)

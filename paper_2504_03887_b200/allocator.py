@@ -227,7 +227,8 @@ def pack_trace(requests: Iterable[dict]) -> PackedTrace:
     return PackedTrace(out, seq_nos, host_errors, kinds_raw)
 
 
-def _raise_status(status: int, index: int, packed: PackedTrace) -> None:
+def _raise_status(status: int, index: int, packed: PackedTrace,
+                  code: int = 0) -> None:
     """Re-raise what the reference raises at request `index`
     (allocator.py:371-385): handle errors wrapped in MalformedSequence,
     ZeroSize unwrapped, unknown kinds as MalformedSequence."""
@@ -247,6 +248,10 @@ def _raise_status(status: int, index: int, packed: PackedTrace) -> None:
     if status == _native.PM_UNKNOWN_HANDLE:
         raise MalformedSequence(str(UnknownHandle(
             f"handle at request {index} never allocated")))
+    if status == _native.PM_INVARIANT_VIOLATION:
+        raise AssertionError(
+            f"allocator invariant violated after request {index}: "
+            f"{_native.INVARIANTS.get(code, code)}")
     if status in (_native.PM_SIZE_LIMIT, _native.PM_BAD_STREAM):
         raise EngineLimitExceeded(
             f"request {index} exceeds the engine's packed ranges")
@@ -261,7 +266,7 @@ def _result_from(rec, packed: PackedTrace, timeline: np.ndarray | None,
     if status == _native.PM_OOM:
         oom_seq = packed.seq_nos[stop]
     elif status != _native.PM_OK:
-        _raise_status(status, stop, packed)
+        _raise_status(status, stop, packed, int(rec["max_free_blocks"]))
     n_ok = stop if status == _native.PM_OOM else len(packed.seq_nos)
     tl = []
     if timeline is not None and n_ok:
@@ -284,12 +289,15 @@ def _result_from(rec, packed: PackedTrace, timeline: np.ndarray | None,
 def replay_batch(traces: Sequence[Iterable[dict]],
                  cfgs: AllocatorConfig | Sequence[AllocatorConfig] | None = None,
                  timeline: bool = True,
-                 result_cls=SimulationResult) -> list:
+                 result_cls=SimulationResult, validate: bool = False) -> list:
     """Replay many independent request lists in one kernel launch.
 
     `cfgs` is one config for all traces or one per trace.  Returns one
     SimulationResult per trace, or raises the first trace's error in the
-    reference's convention.
+    reference's convention.  `validate` runs the validating build of the
+    kernels, which checks the allocator invariants after every request
+    (check_invariants, allocator.py:324-354) and raises AssertionError on a
+    violation, as AllocatorState(validate=True) does.
     """
     packed = [pack_trace(t) for t in traces]
     n = len(packed)
@@ -309,7 +317,8 @@ def replay_batch(traces: Sequence[Iterable[dict]],
             else np.zeros(0, dtype=REQ_DTYPE))
     if n == 0:
         return []
-    results, tl = _native.replay_host_auto(reqs, offsets, cfg_arr, cfg_of, timeline)
+    results, tl = _native.replay_host_auto(reqs, offsets, cfg_arr, cfg_of, timeline,
+                                           validate=validate)
     return [_result_from(results[i], packed[i], tl, int(offsets[i]), result_cls)
             for i in range(n)]
 
@@ -321,12 +330,12 @@ def replay(requests: Iterable[dict], cfg: AllocatorConfig | None = None,
 
     OutOfMemory is a verdict, not an error: the result records the failing
     seq_no and the state reached.  Structural problems (free before alloc,
-    double free, unknown kind) raise MalformedSequence.  `validate` is
-    accepted for signature parity; the kernel's state is checked against
-    the reference's invariants by the parity suite instead of inline.
+    double free, unknown kind) raise MalformedSequence.  `validate=True`
+    checks the allocator invariants after every request on the device
+    (allocator.py:291-292, 319-320, 324-354) and raises AssertionError on a
+    violation.
     """
-    del validate
-    return replay_batch([requests], cfg)[0]
+    return replay_batch([requests], cfg, validate=validate)[0]
 
 
 def load_sequence_file(path: str) -> list[dict]:

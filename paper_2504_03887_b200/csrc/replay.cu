@@ -277,6 +277,18 @@ const char* pm_last_error(void) { return g_last_error.c_str(); }
 
 int pm_version(void) { return 2; }
 
+int pm_validate_inject(int64_t request_index, int32_t kind) {
+#ifdef PM_VALIDATE
+  const int v[2] = {(int)request_index, kind};
+  cudaError_t e = cudaMemcpyToSymbol(pmb::g_inject, v, sizeof(v));
+  return e == cudaSuccess ? PM_SUCCESS : cuda_fail(e, "pm_validate_inject");
+#else
+  (void)request_index;
+  (void)kind;
+  return fail(PM_ERR_INVALID_ARGUMENT, "pm_validate_inject: not a validating build");
+#endif
+}
+
 int pm_replay_workspace_bytes(int64_t total_events, int64_t max_trace_events,
                               int32_t n_traces, size_t* out_bytes) {
   if (!out_bytes || total_events < 0 || max_trace_events < 0 || n_traces < 0)

@@ -155,6 +155,12 @@ struct DirReg {
   __device__ __forceinline__ int count(int d) const {
     return __shfl_sync(kFull, dc, d);
   }
+  __device__ __forceinline__ u64 bound_k(int d) const {
+    return __shfl_sync(kFull, dk, d);
+  }
+  __device__ __forceinline__ u64 bound_a(int d) const {
+    return __shfl_sync(kFull, da, d);
+  }
   __device__ __forceinline__ int count_next(int d) const {
     return __shfl_sync(kFull, dc, d + 1);
   }
@@ -287,6 +293,8 @@ struct DirMem {
   }
   __device__ __forceinline__ int phys(int d) const { return dphys[d]; }
   __device__ __forceinline__ int count(int d) const { return cnt[dphys[d]]; }
+  __device__ __forceinline__ u64 bound_k(int d) const { return dkey[d]; }
+  __device__ __forceinline__ u64 bound_a(int d) const { return daddr[d]; }
   __device__ __forceinline__ int count_next(int d) const {
     return cnt[dphys[d + 1]];
   }
@@ -724,6 +732,121 @@ __device__ __forceinline__ void make_room(const Pool& P, D& dir, Ctx& c,
   }
 }
 
+#ifdef PM_VALIDATE
+// fault injection for the validator's tests: {request index, kind}
+__device__ int g_inject[2];
+
+// ---- invariant checks (validating build) --------------------------------------
+// AllocatorState.check_invariants (allocator.py:324-354) over the wide
+// state after every applied request; see replay_narrow.cuh validate_narrow.
+__device__ __forceinline__ bool live_k(u64 k) { return k != 0ull && k != kFreed; }
+
+template <class D>
+__device__ int validate_wide(const Pool& P, const D& dir, const Recs& rec,
+                             long long n, const Ctx& c, const Cfg& cf, int lane) {
+  const long long align = cf.cp->alignment;
+  const long long cap = cf.cp->device_capacity;
+  int bad = 0;
+  long long free_b = 0, alloc_b = 0;
+  int heads = 0, tails = 0, nfree = 0, free_links = 0, free_refs = 0;
+  auto flag = [&](int code) {
+    if (!bad) bad = code;
+  };
+  for (int d = 0; d < dir.nb; ++d) {
+    const int p = dir.phys(d);
+    const int cntd = dir.count(d);
+    const u64 lk = dir.bound_k(d), la = dir.bound_a(d);
+    const bool last = d + 1 >= dir.nb;
+    const u64 hk = last ? ~0ull : dir.bound_k(d + 1);
+    const u64 ha = last ? ~0ull : dir.bound_a(d + 1);
+    if (lane < cntd) {
+      const int id = p * kBucket + lane;
+      const u64 K = P.key[id], A = P.addr[id], ln = P.links[id];
+      const u64 S = K & kSizeMask;
+      const u32 L = lo32(ln), R = hi32(ln);
+      nfree += 1;
+      free_b += (long long)S;
+      if (S == 0) flag(PM_INV_BLOCK_SIZE);
+      if ((long long)S % align) flag(PM_INV_UNALIGNED);
+      if ((d > 0 && !dir_le(lk, la, K, A)) || (!last && dir_le(hk, ha, K, A)))
+        flag(PM_INV_POOL);
+      for (int side = 0; side < 2; ++side) {
+        const u32 g = side ? R : L;
+        if (g == kNone) {
+          if (side) tails += 1; else heads += 1;
+          continue;
+        }
+        free_links += 1;
+        if (g & kFreeTag) {
+          flag(PM_INV_ADJACENT_FREE);
+          continue;
+        }
+        if ((long long)g >= n) {
+          flag(PM_INV_LINK);
+          continue;
+        }
+        const u64 ga = *rec.word(g, 0), gk = *rec.word(g, 1);
+        const u32 back = (u32)*rec.word(g, side ? 2 : 3);
+        const bool contiguous = side ? A + S == ga : ga + (gk & kSizeMask) == A;
+        if (!live_k(gk) || !contiguous || back != (kFreeTag | (u32)id)) flag(PM_INV_LINK);
+        else if ((gk >> kSizeBits) != (K >> kSizeBits)) flag(PM_INV_STREAM);
+      }
+    }
+  }
+  for (long long h = lane; h < n; h += 32) {
+    const u64 A = *rec.word((u32)h, 0), K = *rec.word((u32)h, 1);
+    if (!live_k(K)) continue;
+    const u64 S = K & kSizeMask;
+    alloc_b += (long long)S;
+    if (S == 0) flag(PM_INV_BLOCK_SIZE);
+    if ((long long)S % align) flag(PM_INV_UNALIGNED);
+    for (int side = 0; side < 2; ++side) {
+      const u32 g = (u32)*rec.word((u32)h, side ? 3 : 2);
+      if (g == kNone) {
+        if (side) tails += 1; else heads += 1;
+        continue;
+      }
+      if (g & kFreeTag) {
+        free_refs += 1;
+        const int id = (int)(g & ~kFreeTag);
+        const u64 ea = P.addr[id], ek = P.key[id], el = P.links[id];
+        const bool ok = side ? (A + S == ea && lo32(el) == (u32)h)
+                             : (ea + (ek & kSizeMask) == A && hi32(el) == (u32)h);
+        if (!ok) flag(PM_INV_LINK);
+        continue;
+      }
+      if ((long long)g >= n) {
+        flag(PM_INV_LINK);
+        continue;
+      }
+      const u64 qa = *rec.word(g, 0), qk = *rec.word(g, 1);
+      const u32 back = (u32)*rec.word(g, side ? 2 : 3);
+      const bool ok = side ? (A + S == qa) : (qa + (qk & kSizeMask) == A);
+      if (!live_k(qk) || !ok || back != (u32)h) flag(PM_INV_LINK);
+      else if ((qk >> kSizeBits) != (K >> kSizeBits)) flag(PM_INV_STREAM);
+    }
+  }
+  const unsigned any = __ballot_sync(kFull, bad != 0);
+  if (any) return __shfl_sync(kFull, bad, __ffs(any) - 1);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    free_b += __shfl_xor_sync(kFull, free_b, o);
+    alloc_b += __shfl_xor_sync(kFull, alloc_b, o);
+  }
+  heads = __reduce_add_sync(kFull, heads);
+  tails = __reduce_add_sync(kFull, tails);
+  nfree = __reduce_add_sync(kFull, nfree);
+  free_links = __reduce_add_sync(kFull, free_links);
+  free_refs = __reduce_add_sync(kFull, free_refs);
+  if (heads != c.nseg || tails != c.nseg) return PM_INV_SEGMENTS;
+  if (nfree != c.F || free_links != free_refs) return PM_INV_POOL;
+  if (alloc_b != c.allocated) return PM_INV_ALLOCATED;
+  if (alloc_b + free_b != c.reserved) return PM_INV_CONSERVATION;
+  if (cap >= 0 && c.reserved > cap) return PM_INV_CAPACITY;
+  return 0;
+}
+#endif
+
 // ---- one trace ---------------------------------------------------------------
 
 template <class D>
@@ -754,6 +877,7 @@ __device__ __forceinline__ void replay_trace(
   c.F = c.maxF = c.nseg = c.nseg_peak = 0;
   int status = PM_OK;
   long long stop = -1;
+  int inv = 0;  // PM_VALIDATE: the violated invariant
 
   const ulonglong2* rq = reinterpret_cast<const ulonglong2*>(reqs + e0);
   ulonglong2 nxt = make_ulonglong2(0ull, 0xFFFFFFFFull);
@@ -988,6 +1112,20 @@ __device__ __forceinline__ void replay_trace(
           }
         }
       }
+#ifdef PM_VALIDATE
+      if (sts == PM_OK && g_inject[1] != 0 && cbase + j == g_inject[0]) {
+        if (g_inject[1] == 1) c.allocated += 1;
+        if (g_inject[1] == 2 && lane == 0 && hj >= 0) *rec.word((u32)hj, 2) = (u64)(u32)hj;
+      }
+      if (sts == PM_OK) {
+        __syncwarp();
+        const int code = validate_wide(P, dir, rec, n, c, cf, lane);
+        if (code) {
+          sts = PM_INVARIANT_VIOLATION;
+          inv = code;
+        }
+      }
+#endif
       if (sts != PM_OK) {
         status = sts;
         stop = cbase + j;
@@ -1021,7 +1159,7 @@ __device__ __forceinline__ void replay_trace(
     res.status = status;
     res.n_segments_final = c.nseg;
     res.n_segments_peak = c.nseg_peak;
-    res.max_free_blocks = c.maxF;
+    res.max_free_blocks = status == PM_INVARIANT_VIOLATION ? inv : c.maxF;
     results[tr] = res;
   }
 }

@@ -134,6 +134,9 @@ struct NDir {
   __device__ __forceinline__ unsigned mask(int d) const {
     return __shfl_sync(kFull, dm, d);
   }
+  __device__ __forceinline__ u64 bound(int d) const {
+    return __shfl_sync(kFull, db, d);
+  }
   __device__ __forceinline__ void set_bit(int d, int b) {
     if (lane == d) dm |= 1u << b;
   }
@@ -253,8 +256,8 @@ struct NDir {
 
 struct NWarpState;
 struct NCtx {
-  long long reserved, allocated;
-  int F;
+  long long reserved, allocated, peak_allocated;
+  int F, maxF;  // free blocks now / high-water mark
   NWarpState* ws;
 };
 
@@ -429,11 +432,10 @@ __device__ __forceinline__ int pool_insert(const NPool& P, D& dir, NCtx& c,
   const int id = dir.phys(d) * kBucket + slot;
   PM_STAT(5);
   c.F += 1;
-  const int mf = max(c.ws->maxF, c.F);  // the count grows only here
+  c.maxF = max(c.maxF, c.F);  // the count grows only here
   __syncwarp();
   P.ka[id] = ka;
   P.ln[id] = links;
-  c.ws->maxF = mf;  // uniform stores
   dir.set_bit(d, slot);
   return id;
 }
@@ -490,16 +492,8 @@ __device__ __forceinline__ int best_fit(const NPool& P, const D& dir,
   const int d = dir.find((u64)ru << 32);
   const int p = dir.phys(d);
   const bool in = (dir.mask(d) >> lane) & 1u;
-  const bool has_next = d + 1 < dir.nb;
-  const int p2 = dir.phys(d + 1);
-  const bool in2 = has_next && ((dir.mask(d + 1) >> lane) & 1u);
-  // both buckets' keys and links in one round of loads: the winner's
-  // entry is then shuffled out, not re-read (an L2 round trip when the
-  // entries live in HBM)
   const u64 ka = in ? P.ka[p * kBucket + lane] : ~0ull;
-  const u64 ka2 = in2 ? P.ka[p2 * kBucket + lane] : ~0ull;
   const u64 ln = in ? P.ln[p * kBucket + lane] : 0ull;
-  const u64 ln2 = in2 ? P.ln[p2 * kBucket + lane] : 0ull;
   PM_STAT(8);
   const bool el = in && hi(ka) >= ru && hi(ka) - ru < span;
   const int w = argmin_pk(el, ka);
@@ -508,14 +502,19 @@ __device__ __forceinline__ int best_fit(const NPool& P, const D& dir,
     LN = __shfl_sync(kFull, ln, w);
     return p * kBucket + w;
   }
+  // every key of the next bucket is >= (ru, 0): its minimum is the only
+  // candidate (loaded only now: most allocations hit the first bucket)
   PM_STAT(9);
+  if (d + 1 >= dir.nb) return -1;
+  const int p2 = dir.phys(d + 1);
+  const bool in2 = (dir.mask(d + 1) >> lane) & 1u;
+  const u64 ka2 = in2 ? P.ka[p2 * kBucket + lane] : ~0ull;
   const int w2 = argmin_pk(in2, ka2);
   if (w2 >= 0) {
     const u64 kw = __shfl_sync(kFull, ka2, w2);
-    const u64 lw = __shfl_sync(kFull, ln2, w2);
     if (hi(kw) - ru < span) {
       KA = kw;
-      LN = lw;
+      LN = P.ln[p2 * kBucket + w2];
       return p2 * kBucket + w2;
     }
   }
@@ -577,6 +576,130 @@ __device__ __forceinline__ void make_room(const NPool& P, D& dir, NCtx& c,
     __syncwarp();
   }
 }
+
+#ifdef PM_VALIDATE
+// ---- invariant checks (validating build) --------------------------------------
+//
+// AllocatorState.check_invariants (allocator.py:324-354) over the narrow
+// state, after every applied request: every free entry and every live
+// record is checked against its neighbours (mutual refs, address
+// contiguity, no free-free adjacency), the index ranges, the chain heads /
+// tails against the segment count, and the byte sums against reserved /
+// allocated.  Returns 0 or a pm_invariant_t code.
+
+__device__ __forceinline__ long long warp_sum64(long long v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+  return v;
+}
+__device__ __forceinline__ int warp_sum32(int v) { return __reduce_add_sync(kFull, v); }
+__device__ __forceinline__ bool live_u(u32 y) { return y != 0u && y != kFreedU; }
+
+template <class D>
+__device__ int validate_narrow(const NPool& P, const D& dir, const NRecs& rec,
+                               int wm, const NCtx& c, const NWarpState* ws, int s,
+                               int lane) {
+  const long long align = ws->cp->alignment;
+  const long long cap = ws->cp->device_capacity;
+  int bad = 0;
+  long long free_u = 0, alloc_u = 0;
+  int heads = 0, tails = 0, nfree = 0, free_links = 0, free_refs = 0;
+  auto flag = [&](int code) {
+    if (!bad) bad = code;
+  };
+  // neighbour `g` of a free entry `id` at [A, A+S): an allocated handle whose
+  // opposite ref names the entry
+  auto check_free_nb = [&](u32 g, int id, u32 A, u32 S, bool right) {
+    if (g & kFreeTag) {
+      flag(PM_INV_ADJACENT_FREE);
+      return;
+    }
+    if ((int)g > wm) {
+      flag(PM_INV_LINK);
+      return;
+    }
+    const uint4 r = *rec.rec(g);
+    const bool contiguous = right ? A + S == r.x : r.x + r.y == A;
+    const u32 back = right ? r.z : r.w;
+    if (!live_u(r.y) || !contiguous || back != (kFreeTag | (u32)id)) flag(PM_INV_LINK);
+  };
+  for (int d = 0; d < dir.nb; ++d) {
+    const int p = dir.phys(d);
+    const unsigned m = dir.mask(d);
+    const u64 lo_b = dir.bound(d);
+    const bool last = d + 1 >= dir.nb;
+    const u64 hi_b = last ? ~0ull : dir.bound(d + 1);
+    if ((m >> lane) & 1u) {
+      const int id = p * kBucket + lane;
+      const u64 ka = P.ka[id], ln = P.ln[id];
+      const u32 S = hi(ka), A = lo(ka), L = lo(ln), R = hi(ln);
+      nfree += 1;
+      free_u += S;
+      if (S == 0) flag(PM_INV_BLOCK_SIZE);
+      if ((((long long)S) << s) % align) flag(PM_INV_UNALIGNED);
+      if (ka < lo_b || (!last && ka >= hi_b)) flag(PM_INV_POOL);
+      if (L == kNone) {
+        heads += 1;
+      } else {
+        free_links += 1;
+        check_free_nb(L, id, A, S, false);
+      }
+      if (R == kNone) {
+        tails += 1;
+      } else {
+        free_links += 1;
+        check_free_nb(R, id, A, S, true);
+      }
+    }
+  }
+  for (int h = lane; h <= wm; h += 32) {
+    const uint4 r = *rec.rec((u32)h);
+    if (!live_u(r.y)) continue;
+    alloc_u += r.y;
+    if ((((long long)r.y) << s) % align) flag(PM_INV_UNALIGNED);
+    for (int side = 0; side < 2; ++side) {
+      const u32 g = side ? r.w : r.z;
+      if (g == kNone) {
+        if (side) tails += 1; else heads += 1;
+        continue;
+      }
+      if (g & kFreeTag) {
+        // a free neighbour: its entry must name h back and abut it
+        free_refs += 1;
+        const int id = (int)(g & ~kFreeTag);
+        const u64 ka = P.ka[id], ln = P.ln[id];
+        const bool ok = side ? (r.x + r.y == lo(ka) && lo(ln) == (u32)h)
+                             : (lo(ka) + hi(ka) == r.x && hi(ln) == (u32)h);
+        if (!ok) flag(PM_INV_LINK);
+        continue;
+      }
+      if ((int)g > wm) {
+        flag(PM_INV_LINK);
+        continue;
+      }
+      const uint4 q = *rec.rec(g);
+      const bool ok = side ? (r.x + r.y == q.x && q.z == (u32)h)
+                           : (q.x + q.y == r.x && q.w == (u32)h);
+      if (!live_u(q.y) || !ok) flag(PM_INV_LINK);
+    }
+  }
+  const unsigned any = __ballot_sync(kFull, bad != 0);
+  if (any) return __shfl_sync(kFull, bad, __ffs(any) - 1);
+  heads = warp_sum32(heads);
+  tails = warp_sum32(tails);
+  nfree = warp_sum32(nfree);
+  free_links = warp_sum32(free_links);
+  free_refs = warp_sum32(free_refs);
+  free_u = warp_sum64(free_u);
+  alloc_u = warp_sum64(alloc_u);
+  if (heads != ws->nseg || tails != ws->nseg) return PM_INV_SEGMENTS;
+  if (nfree != c.F || free_links != free_refs) return PM_INV_POOL;
+  if ((alloc_u << s) != c.allocated) return PM_INV_ALLOCATED;
+  if (((alloc_u + free_u) << s) != c.reserved) return PM_INV_CONSERVATION;
+  if (cap >= 0 && c.reserved > cap) return PM_INV_CAPACITY;
+  return 0;
+}
+#endif
 
 // ---- request staging: 1-D TMA bulk copies into a per-warp double buffer ----
 
@@ -699,11 +822,12 @@ __device__ __forceinline__ void replay_trace(
   __syncwarp();
 
   NCtx c;
-  c.reserved = c.allocated = 0;
-  c.F = 0;
+  c.reserved = c.allocated = c.peak_allocated = 0;
+  c.F = c.maxF = 0;
   c.ws = ws;
   int status = PM_OK;
   int stop = -1;
+  int inv = 0;  // PM_VALIDATE: the violated invariant
   // A trace of >= 2^20 requests replays at one warp's latency (~1 us per
   // request) in every pass, and long traces are the ones that outgrow the
   // earlier passes' capacity and restart: send it straight to the last
@@ -802,6 +926,11 @@ __device__ __forceinline__ void replay_trace(
     uint4 r = make_uint4(0, 0, 0, 0);
     uint4* const myrec = rec.rec((u32)(hok ? my_h : 0));
     if (hok && !fresh) r = *myrec;
+#ifdef PM_VALIDATE
+    // the validator reads every record <= wm: a fresh handle's record is
+    // "never allocated" from the start of its chunk
+    if (fresh) *myrec = r;
+#endif
     uint4* st = sg.rec;
     st[lane] = r;
     const int hcmp = hok ? my_h : -1;
@@ -1012,9 +1141,7 @@ __device__ __forceinline__ void replay_trace(
           __syncwarp();
           if (is_alloc) {
             c.allocated += (long long)out_s << s;
-            const long long pa = max(ws->peak_allocated, c.allocated);
-            __syncwarp();
-            ws->peak_allocated = pa;  // uniform store
+            c.peak_allocated = max(c.peak_allocated, c.allocated);
             if (lane == j) {
               const uint4 o = make_uint4(out_a, out_s, out_L, out_R);
               st[j] = o;
@@ -1026,6 +1153,22 @@ __device__ __forceinline__ void replay_trace(
           }
         }
       }
+#ifdef PM_VALIDATE
+      if (sts == PM_OK && pmb::g_inject[1] != 0 && cbase + j == pmb::g_inject[0]) {
+        // fault injection for the validator's own tests (pm_validate_inject)
+        if (pmb::g_inject[1] == 1) c.allocated += 1ll << s;
+        if (pmb::g_inject[1] == 2 && lane == 0 && hj >= 0)
+          *rec.word((u32)hj, 2) = (u32)hj;  // a ref that is not mutual
+      }
+      if (sts == PM_OK) {
+        __syncwarp();
+        const int code = validate_narrow(P, dir, rec, wm, c, ws, s, lane);
+        if (code) {
+          sts = PM_INVARIANT_VIOLATION;
+          inv = code;
+        }
+      }
+#endif
       if (sts != PM_OK) {
         status = sts;
         stop = cbase + j;
@@ -1083,7 +1226,7 @@ __device__ __forceinline__ void replay_trace(
   if (lane == 0) {
     pm_result_t res;
     res.peak_reserved = ws->peak_reserved;
-    res.peak_allocated = ws->peak_allocated;
+    res.peak_allocated = c.peak_allocated;
     res.final_reserved = c.reserved;
     res.final_allocated = c.allocated;
     res.stop_index = stop;
@@ -1092,7 +1235,7 @@ __device__ __forceinline__ void replay_trace(
     res.status = status;
     res.n_segments_final = ws->nseg;
     res.n_segments_peak = ws->nseg_peak;
-    res.max_free_blocks = ws->maxF;
+    res.max_free_blocks = status == PM_INVARIANT_VIOLATION ? inv : c.maxF;
     results[tr] = res;
   }
 }
@@ -1190,6 +1333,7 @@ struct NDirMem {
   }
   __device__ __forceinline__ int phys(int d) const { return dp[d]; }
   __device__ __forceinline__ unsigned mask(int d) const { return m[d]; }
+  __device__ __forceinline__ u64 bound(int d) const { return db[d]; }
   __device__ __forceinline__ void set_mask(int d, unsigned v) {
     __syncwarp();
     m[d] = v;  // uniform store

@@ -54,7 +54,7 @@ def test_digest_error_surfaces_after_the_pipeline(monkeypatch):
     monkeypatch.setattr(est_mod, "build_sequence",
                         lambda a, iterations: calls.append("build") or Seq())
     monkeypatch.setattr(est_mod, "replay_sequence",
-                        lambda s, cfg, timeline=True: calls.append(("replay", timeline)) or Res())
+                        lambda s, cfg, timeline=True, validate=False: calls.append(("replay", timeline)) or Res())
     monkeypatch.setattr(PeakMemoryEstimator, "_digest",
                         lambda self, *a: (_ for _ in ()).throw(ValueError("digest")))
 
