@@ -50,7 +50,17 @@ from .analysis import (
 )
 from .estimator import EstimateReport, PeakMemoryEstimator
 from .linking import LayerMemoryProfile, link
-from .metrics import predict_oom
+from .metrics import (
+    EvalJob,
+    MetricSet,
+    Quadrant,
+    ValidationRecord,
+    aggregate,
+    evaluate,
+    evaluate_columns,
+    evaluate_sweep,
+    predict_oom,
+)
 from .orchestration import (
     AnalyzedTrace,
     MemoryRequest,
