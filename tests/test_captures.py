@@ -63,3 +63,44 @@ def test_capture_pipeline_matches_reference(name, tmp_path):
     want = golden("captures_golden.json")[name]
     for key in want:
         assert got[key] == want[key], key
+
+
+# ---- C2 as BASELINE.json states it: 64 GPT-2 small traces, bs 1..64 --------
+
+def c2_sweep():
+    z = np.load(GOLDEN / "c2_sweep.npz")
+    return z["reqs"], z["offsets"], golden("c2_sweep_golden.json")["traces"]
+
+
+def check_sweep(res, tl, offs, meta):
+    from conftest import digest
+    assert len(meta) == 64 and [m["batch"] for m in meta] == list(range(1, 65))
+    check_results(res, meta)
+    for i, m in enumerate(meta):
+        assert int(res[i]["n_events_replayed"]) == m["n_requests"] == m["timeline_len"]
+        if tl is not None:
+            pairs = tl[2 * offs[i]: 2 * offs[i + 1]].reshape(-1, 2).tolist()
+            rows = [[k, a, b] for k, (a, b) in enumerate(pairs)]
+            assert digest(rows) == m["timeline_sha256"], m["name"]
+
+
+def test_c2_sweep_oracle():
+    reqs, offs, meta = c2_sweep()
+    res, tl = oracle.replay_batch(reqs, offs, cfg_record(AllocatorConfig()),
+                                  timeline=True)
+    check_sweep(res, tl, offs, meta)
+    # the sweep is what it claims: 64 different peaks growing with batch size
+    peaks = [m["peak_reserved"] for m in meta]
+    assert len(set(peaks)) == 64 and peaks[-1] > 8 * peaks[0]
+
+
+@pytest.mark.gpu
+@pytest.mark.usefixtures("require_gpu")
+def test_c2_sweep_gpu_one_batch():
+    """All 64 orchestrated GPT-2 sequences replayed as ONE batch on the GPU,
+    bit-exact against the reference (peaks, finals, segment counts, full
+    timelines)."""
+    from paper_2504_03887_b200 import _native
+    reqs, offs, meta = c2_sweep()
+    res, tl = _native.replay_host(reqs, offs, cfg_record(AllocatorConfig()), None, True)
+    check_sweep(res, tl, offs, meta)
