@@ -38,12 +38,14 @@ constexpr int kNarrowWarps = 24;  // narrow main kernel (PM_REPLAY_WARPS: 12..32
 constexpr size_t kBucket_host = 32;  // warps (traces in flight) per CTA, 1 CTA / SM
 constexpr int kRetryWarps = 1;
 constexpr int kMaxRetryWarps = 64;
+constexpr int kPass1Warps = 6;    // narrow pass 1: warps (private pools) per SM
 
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
-// workspace = ctl | retry list | retry pools | record table
+// workspace = ctl | retry list | retry pools | record table | checkpoint
+// offsets | checkpoint region
 struct Layout {
-  size_t retry_list, gpool, recs, total;
+  size_t retry_list, gpool, recs, ck_off, ck, ck_bytes, total;
   int nbmax_g;
   int retry_warps;
 };
@@ -53,7 +55,7 @@ Layout layout_for(int64_t total_events, int64_t max_trace_events,
   Layout L;
   size_t off = align_up(sizeof(pmb::Ctl), 256);
   L.retry_list = off;
-  off = align_up(off + 6 * sizeof(int32_t) * (size_t)(n_traces > 0 ? n_traces : 1),
+  off = align_up(off + 7 * sizeof(int32_t) * (size_t)(n_traces > 0 ? n_traces : 1),
                  256);
   const int64_t mx = max_trace_events > 0 ? max_trace_events : 1;
   L.nbmax_g = (int)(mx / 8 + 4);
@@ -64,6 +66,17 @@ Layout layout_for(int64_t total_events, int64_t max_trace_events,
   off = align_up(off + (size_t)warps * pmb::gmem_warp_bytes(L.nbmax_g), 256);
   L.recs = off;
   off = align_up(off + 32 * (size_t)(total_events > 0 ? total_events : 1), 256);
+  // checkpoints of traces handed between narrow passes (replay_narrow.cuh
+  // NCk): ~16 B per free block; a full region only means a restart
+  L.ck_off = off;
+  off = align_up(off + 8 * (size_t)(n_traces > 0 ? n_traces : 1), 256);
+  L.ck = off;
+  size_t ckb = 4 * (size_t)(total_events > 0 ? total_events : 1) +
+               256 * (size_t)(n_traces > 0 ? n_traces : 1);
+  if (ckb < (64u << 20)) ckb = 64u << 20;
+  if (ckb > (1ull << 30)) ckb = 1ull << 30;
+  L.ck_bytes = ckb;
+  off = align_up(off + ckb, 256);
   L.total = off;
   return L;
 }
@@ -74,8 +87,10 @@ struct Occupancy {
   bool narrow = true;  // main pass: replay_narrow_kernel (else the wide kernel)
   int per_sm_n = 0, buckets_n = 0;  // the narrow main kernel's launch
   size_t smem_n = 0;
-  int nbmax_m1 = 0, nbmax_m2 = 0;   // narrow memory-directory passes 1-2
+  int nbmax_m1 = 0, nbmax_m2 = 0;   // narrow memory-directory passes 2-3
   size_t smem_m1 = 0;
+  int warps_s1 = 0, nbmax_s1 = 0;   // pass 1: warps per SM, buckets per warp
+  size_t warp_bytes_s1 = 0;
   int per_sm1 = 0;  // tier-1 retry kernel
   size_t smem1 = 0;
   int nbmax2 = 0;   // tier-2: one warp with a shared-memory directory
@@ -180,11 +195,17 @@ int query_occupancy(Occupancy* out) {
     // per bucket, + 512 B of entries per bucket in the shared-memory pass
     o.nbmax_m1 = (int)(((size_t)optin - pmn::kWarpStageBytes - 256) / (24 + 512));
     o.smem_m1 = pmn::mem_tier_smem(o.nbmax_m1, true);
-    o.nbmax_m2 = (int)(((size_t)optin - pmn::kWarpStageBytes - 256) / 24);
+    o.warps_s1 = kPass1Warps;
+    if (const char* env = getenv("PM_PASS1_WARPS")) o.warps_s1 = atoi(env);
+    if (o.warps_s1 < 1) o.warps_s1 = 1;
+    if (o.warps_s1 > 8) o.warps_s1 = 8;
+    o.nbmax_s1 = (int)(((size_t)optin / o.warps_s1 - pmn::kWarpStageBytes - 256) / (24 + 512));
+    o.warp_bytes_s1 = align_up(pmn::mem_tier_smem(o.nbmax_s1, true), 128);
     e = cudaFuncSetAttribute(pmn::replay_narrow_mem_kernel<true>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)o.smem_m1);
+                             (int)std::max(o.smem_m1, o.warps_s1 * o.warp_bytes_s1));
     if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute pass 1");
+    o.nbmax_m2 = (int)(((size_t)optin - pmn::kWarpStageBytes - 256) / 24);
     e = cudaFuncSetAttribute(pmn::replay_narrow_mem_kernel<false>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)pmn::mem_tier_smem(o.nbmax_m2, false));
@@ -334,6 +355,9 @@ int replay_batch_impl(const pm_req_t* reqs, const int64_t* trace_offsets,
   int32_t* retry_list = reinterpret_cast<int32_t*>(base + L.retry_list);
   char* gpool = base + L.gpool;
   pmb::u64* recs = reinterpret_cast<pmb::u64*>(base + L.recs);
+  long long* ck_off = reinterpret_cast<long long*>(base + L.ck_off);
+  char* ck_base = base + L.ck;
+  const unsigned long long ck_cap = L.ck_bytes;
 
   Occupancy occ;
   int rc = query_occupancy(&occ);
@@ -344,12 +368,13 @@ int replay_batch_impl(const pm_req_t* reqs, const int64_t* trace_offsets,
   // pass lists (pmn::route): narrow memory-directory tiers, then the wide
   // tiers 1-4 (an encoding limit goes straight to wide tier 1)
   const size_t nt = (size_t)n_traces;
-  int32_t* list_m1 = retry_list;           // pass 1: narrow, smem entries
-  int32_t* list_m2 = retry_list + nt;      // pass 2: narrow, HBM entries
-  int32_t* list_w1 = retry_list + 2 * nt;  // pass 3: wide tier 1
-  int32_t* list_w2 = retry_list + 3 * nt;  // pass 4: wide tier 2
-  int32_t* list_w3 = retry_list + 4 * nt;  // pass 5: wide tier 3
-  int32_t* list_w4 = retry_list + 5 * nt;  // pass 6: wide tier 4
+  int32_t* list_m1 = retry_list;           // pass 1: narrow, smem, multi-warp
+  int32_t* list_mb = retry_list + nt;      // pass 2: narrow, smem, one warp
+  int32_t* list_m2 = retry_list + 2 * nt;  // pass 3: narrow, HBM entries
+  int32_t* list_w1 = retry_list + 3 * nt;  // pass 4: wide tier 1
+  int32_t* list_w2 = retry_list + 4 * nt;  // pass 5: wide tier 2
+  int32_t* list_w3 = retry_list + 5 * nt;  // pass 6: wide tier 3
+  int32_t* list_w4 = retry_list + 6 * nt;  // pass 7: wide tier 4
   const bool narrow = occ.narrow || wire != nullptr;  // wire words need it
   const int mwarps = narrow && !occ.narrow ? kNarrowWarps : occ.warps;
   long long want = ((long long)n_traces + mwarps - 1) / mwarps;
@@ -369,7 +394,7 @@ int replay_batch_impl(const pm_req_t* reqs, const int64_t* trace_offsets,
       reinterpret_cast<pmb::u32*>(recs), ctl, trace_order, n_traces, list_m1, \
       occ.buckets_n, group_end, n_groups, ready,                             \
       reinterpret_cast<const pmb::u64*>(wire), const_cast<pm_req_t*>(reqs),   \
-      list_w1, long_trace)
+      list_w1, long_trace, ck_off, ck_base, ck_cap)
 #define PM_LAUNCH_MAIN(W)                                                     \
   pmb::replay_smem_kernel<W><<<(unsigned)grid, W * 32, occ.smem, stream>>>(  \
       reqs, trace_offsets, cfgs, cfg_of_trace, results, timeline, recs, ctl, \
@@ -402,13 +427,25 @@ int replay_batch_impl(const pm_req_t* reqs, const int64_t* trace_offsets,
   const long long gtraces = n_traces < occ.sms ? n_traces : occ.sms;
   // passes 1-2: narrow, shared-memory directory (entries in shared memory,
   // then in HBM: the per-CTA region fits in tier 4's, nb <= nbmax_g)
-  pmn::replay_narrow_mem_kernel<true><<<(unsigned)gtraces, 32, occ.smem_m1, stream>>>(
-      reqs, trace_offsets, cfgs, cfg_of_trace, results, timeline,
-      reinterpret_cast<pmb::u32*>(recs), ctl, pmn::kTierMemSmem, list_m1, list_m2,
-      list_w1, nullptr, occ.nbmax_m1, reinterpret_cast<const pmb::u64*>(wire),
-      const_cast<pm_req_t*>(reqs), long_trace);
+  // pass 1: several warps per SM, each with a private shared-memory pool
+  // (fragmented traces replay side by side); pass 2: one warp owning the
+  // SM's shared memory for the traces that outgrow those
+  pmn::replay_narrow_mem_kernel<true>
+      <<<(unsigned)gtraces, 32 * occ.warps_s1, occ.warps_s1 * occ.warp_bytes_s1, stream>>>(
+          reqs, trace_offsets, cfgs, cfg_of_trace, results, timeline,
+          reinterpret_cast<pmb::u32*>(recs), ctl, pmn::kTierMemSmem, list_m1, list_mb,
+          list_w1, nullptr, occ.nbmax_s1, reinterpret_cast<const pmb::u64*>(wire),
+          const_cast<pm_req_t*>(reqs), long_trace, ck_off, ck_base, ck_cap,
+          occ.warp_bytes_s1);
   e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "replay pass-1 launch");
+  pmn::replay_narrow_mem_kernel<true><<<(unsigned)gtraces, 32, occ.smem_m1, stream>>>(
+      reqs, trace_offsets, cfgs, cfg_of_trace, results, timeline,
+      reinterpret_cast<pmb::u32*>(recs), ctl, pmn::kTierMemSmemBig, list_mb, list_m2,
+      list_w1, nullptr, occ.nbmax_m1, reinterpret_cast<const pmb::u64*>(wire),
+      const_cast<pm_req_t*>(reqs), long_trace, ck_off, ck_base, ck_cap, 0);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "replay pass-2 launch");
   {
     const int nbm2 = occ.nbmax_m2 < L.nbmax_g ? occ.nbmax_m2 : L.nbmax_g;
     // up to one CTA per SM, as many as the retry region holds
@@ -421,9 +458,9 @@ int replay_batch_impl(const pm_req_t* reqs, const int64_t* trace_offsets,
             reqs, trace_offsets, cfgs, cfg_of_trace, results, timeline,
             reinterpret_cast<pmb::u32*>(recs), ctl, pmn::kTierMemHbm, list_m2,
             list_w4, list_w1, gpool, nbm2, reinterpret_cast<const pmb::u64*>(wire),
-            const_cast<pm_req_t*>(reqs), pmn::kNoSkip);
+            const_cast<pm_req_t*>(reqs), pmn::kNoSkip, ck_off, ck_base, ck_cap, 0);
     e = cudaGetLastError();
-    if (e != cudaSuccess) return cuda_fail(e, "replay pass-2 launch");
+    if (e != cudaSuccess) return cuda_fail(e, "replay pass-3 launch");
   }
   // wide tier 1 (pass 3): dedicated 32-bucket pools (grid sized for the
   // worst case; idle CTAs exit at once when nothing was escalated)

@@ -1169,7 +1169,8 @@ __device__ __forceinline__ void replay_trace(
 struct Ctl {
   unsigned work[8];   // work counters: main pass, tiers 1..4
   unsigned n_list[8]; // traces queued for tier k (index 1..4)
-  unsigned pad[48];
+  unsigned long long ck_used;  // checkpoint region bump counter (narrow passes)
+  unsigned pad[46];
 };
 
 // Shared-memory layout of the main kernel (per CTA): the bucket pool

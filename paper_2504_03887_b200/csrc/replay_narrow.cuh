@@ -109,6 +109,7 @@ struct NRecs {
 // slots except on bucket split / merge, so their ids stay valid and the
 // allocated neighbours' refs need no re-pointing.
 struct NDir {
+  static constexpr bool kResumes = false;  // the main pass starts traces fresh
   u64 db;
   int dp;
   unsigned dm;
@@ -274,6 +275,8 @@ struct __align__(16) NWarpState {
   long long peak_reserved, peak_allocated;
   u32 next_base;  // units
   int nseg, nseg_peak, maxF;  // maxF: free-block high-water mark
+  u64 stash_ka, stash_ln;     // a free entry the pool had no room for
+  int abase_chunk;            // wire: allocs before the current chunk
 };
 
 // Per-warp staging area: two 512 B request buffers (TMA destinations), 512 B
@@ -407,27 +410,54 @@ __device__ __forceinline__ bool split_bucket(const NPool& P, D& dir, int d,
   return true;
 }
 
-// Insert a free block; returns its id or -1 on pool overflow.
+// The pool cannot take an entry (no physical bucket, a full directory): the
+// request still completes -- the entry is parked in the warp's state under
+// kStashId and the trace is handed to the next pass right after this
+// request, its checkpoint carrying the parked entry (save_checkpoint).
+constexpr int kStashId = 0x7FFFFFF0;
+
+__device__ __forceinline__ int stash_entry(NCtx& c, u64 ka, u64 links) {
+  c.F += 1;
+  c.maxF = max(c.maxF, c.F);
+  __syncwarp();
+  c.ws->stash_ka = ka;  // uniform stores
+  c.ws->stash_ln = links;
+  __syncwarp();
+  return kStashId;
+}
+
+// Insert a free block; returns its id (kStashId: parked, see above).
 template <class D>
 __device__ __forceinline__ int pool_insert(const NPool& P, D& dir, NCtx& c,
                                            u64 ka, u64 links, const NRecs& rec,
                                            uint4* st, int hcmp, int lane) {
+  bool room = true;
   if (dir.nb == 0) {
     const int q = dir.alloc_phys_wait();
-    if (q < 0) return -1;
-    dir.insert(0, 0ull, q, 0u);
+    if (q < 0)
+      room = false;
+    else
+      dir.insert(0, 0ull, q, 0u);
   }
-  int d = dir.find(ka);
-  unsigned m = dir.mask(d);
-  while (m == kFull) {
-    // a full directory whose buckets are >= 3/4 occupied would thrash
-    // (merge a pair, split, merge ...) on every insert: hand the trace to
-    // the next pass, which has room, instead
-    if (dir.full() && c.F >= 24 * dir.capacity()) return -1;
-    if (!split_bucket(P, dir, d, rec, st, hcmp, lane)) return -1;
+  int d = 0;
+  unsigned m = 0;
+  if (room) {
     d = dir.find(ka);
     m = dir.mask(d);
+    while (m == kFull) {
+      // a full directory whose buckets are >= 3/4 occupied would thrash
+      // (merge a pair, split, merge ...) on every insert: hand the trace to
+      // the next pass, which has room, instead
+      if ((dir.full() && c.F >= 24 * dir.capacity()) ||
+          !split_bucket(P, dir, d, rec, st, hcmp, lane)) {
+        room = false;
+        break;
+      }
+      d = dir.find(ka);
+      m = dir.mask(d);
+    }
   }
+  if (!room) return stash_entry(c, ka, links);
   const int slot = __ffs(~m) - 1;
   const int id = dir.phys(d) * kBucket + slot;
   PM_STAT(5);
@@ -756,6 +786,176 @@ __device__ __forceinline__ int ctz64(long long v) {
   return __ffsll(v) - 1;
 }
 
+// ---- checkpoints: hand a trace to the next pass mid-way ---------------------
+//
+// A trace handed off between requests (prepare_request) leaves its complete
+// state behind: the scalars, the watermark and, bucket by bucket in
+// directory order, its free entries -- the record table already lives in
+// HBM.  The next narrow pass rebuilds the same bucket partition in its own
+// pool (only the entries' ids change: their allocated neighbours' refs are
+// re-pointed) and continues at the next request instead of replaying the
+// trace again from request 0.  Space comes from a bump region of the
+// workspace; when it is exhausted the trace simply restarts, as before.
+
+struct __align__(16) NCkHeader {
+  int r, wm, abase, nb;
+  int F, maxF, nseg, nseg_peak;
+  long long reserved, allocated, peak_allocated, peak_reserved;
+  u32 next_base, pad0, pad1, pad2;
+};  // 80 B
+
+struct NCk {
+  long long* off;                  // per trace: checkpoint offset or -1
+  char* base;                      // bump region
+  unsigned long long* used;        // bump counter (Ctl)
+  unsigned long long cap;          // region bytes
+  bool save, load;                 // this pass writes / resumes checkpoints
+};
+
+template <class D>
+__device__ __forceinline__ void save_checkpoint(const NCk& ck, int tr, int r, int wm,
+                                                int abase, const NCtx& c,
+                                                const NWarpState* ws, const NPool& P,
+                                                const D& dir, int lane) {
+  // the parked entry (counted in c.F) joins the bucket whose key range
+  // holds it -- or forms the only group of an empty directory
+  const u64 sk = ws->stash_ka, sl = ws->stash_ln;
+  const int groups = dir.nb > 0 ? dir.nb : 1;
+  const unsigned long long bytes =
+      sizeof(NCkHeader) + 16ull * (unsigned long long)groups + 16ull * (unsigned long long)c.F;
+  unsigned long long off = 0;
+  if (lane == 0) off = atomicAdd(ck.used, (bytes + 15) & ~15ull);
+  off = __shfl_sync(kFull, off, 0);
+  if (off + bytes > ck.cap) {
+    if (lane == 0) ck.off[tr] = -1;  // no room: the next pass restarts it
+    return;
+  }
+  char* b = ck.base + off;
+  if (lane == 0) {
+    NCkHeader h;
+    h.r = r;
+    h.wm = wm;
+    h.abase = abase;
+    h.nb = groups;
+    h.F = c.F;
+    h.maxF = c.maxF;
+    h.nseg = ws->nseg;
+    h.nseg_peak = ws->nseg_peak;
+    h.reserved = c.reserved;
+    h.allocated = c.allocated;
+    h.peak_allocated = c.peak_allocated;
+    h.peak_reserved = ws->peak_reserved;
+    h.next_base = ws->next_base;
+    h.pad0 = h.pad1 = h.pad2 = 0;
+    *reinterpret_cast<NCkHeader*>(b) = h;
+  }
+  ulonglong2* desc = reinterpret_cast<ulonglong2*>(b + sizeof(NCkHeader));
+  ulonglong2* ent = desc + groups;
+  int e = 0;
+  if (dir.nb == 0) {
+    if (lane == 0) {
+      desc[0] = make_ulonglong2(0ull, 1ull);
+      ent[0] = make_ulonglong2(sk, sl);
+    }
+  }
+  for (int d = 0; d < dir.nb; ++d) {
+    const int p = dir.phys(d);
+    const unsigned m = dir.mask(d);
+    const u64 bound = dir.bound(d);
+    const bool last = d + 1 >= dir.nb;
+    const u64 next = last ? ~0ull : dir.bound(d + 1);
+    const bool here = sk >= bound && (last || sk < next);
+    const int k = __popc(m) + (here ? 1 : 0);
+    if (lane == 0) desc[d] = make_ulonglong2(bound, (u64)k);
+    if ((m >> lane) & 1u) {
+      const int r = __popc(m & lanemask_lt());
+      ent[e + r] = make_ulonglong2(P.ka[p * kBucket + lane], P.ln[p * kBucket + lane]);
+    }
+    if (here && lane == 0) ent[e + k - 1] = make_ulonglong2(sk, sl);
+    e += k;
+  }
+  __threadfence();  // the next pass (a later launch) reads it
+  if (lane == 0) ck.off[tr] = (long long)off;
+}
+
+// Rebuild the directory from a checkpoint (a fresh pass: empty directory,
+// private pool) and re-point the entries' allocated neighbours.  Returns the
+// request to continue at.
+template <class D>
+__device__ __forceinline__ int resume_state(const NCk& ck, int tr, NCtx& c,
+                                            NWarpState* ws, const NPool& P, D& dir,
+                                            const NRecs& rec, int& wm, int& abase,
+                                            int lane) {
+  const char* b = ck.base + ck.off[tr];
+  const NCkHeader h = *reinterpret_cast<const NCkHeader*>(b);
+  const ulonglong2* desc = reinterpret_cast<const ulonglong2*>(b + sizeof(NCkHeader));
+  const ulonglong2* ent = desc + h.nb;
+  int e = 0, pos = 0;
+  auto relink = [&](const ulonglong2& x, int id) {
+    const u32 L = lo(x.y), R = hi(x.y);
+    const u32 val = kFreeTag | (u32)id;
+    if (L != kNone) *rec.word(L, 3) = val;
+    if (R != kNone) *rec.word(R, 2) = val;
+  };
+  for (int d = 0; d < h.nb; ++d) {
+    const ulonglong2 dd = desc[d];
+    const int k = (int)dd.y;
+    const int p = dir.alloc_phys();  // a fresh pass holds >= nb + 1 buckets
+    if (k <= kBucket) {
+      const int id = p * kBucket + lane;
+      if (lane < k) {
+        const ulonglong2 x = ent[e + lane];
+        P.ka[id] = x.x;
+        P.ln[id] = x.y;
+        relink(x, id);
+      }
+      __syncwarp();
+      dir.insert(pos++, dd.x, p, k >= 32 ? kFull : ((1u << k) - 1u));
+    } else {
+      // a full bucket plus the parked entry: 33 keys, split at rank 16
+      const ulonglong2 x = ent[e + lane];
+      const ulonglong2 xe = ent[e + kBucket];
+      int rank = xe.x < x.x ? 1 : 0;
+#pragma unroll 8
+      for (int i = 0; i < kBucket; ++i) rank += __shfl_sync(kFull, x.x, i) < x.x ? 1 : 0;
+      const int rank_e = __popc(__ballot_sync(kFull, x.x < xe.x));
+      const int q = dir.alloc_phys();
+      const int id = rank < kHalf ? p * kBucket + rank : q * kBucket + rank - kHalf;
+      P.ka[id] = x.x;
+      P.ln[id] = x.y;
+      relink(x, id);
+      const int ide = rank_e < kHalf ? p * kBucket + rank_e : q * kBucket + rank_e - kHalf;
+      if (lane == 0) {
+        P.ka[ide] = xe.x;
+        P.ln[ide] = xe.y;
+        relink(xe, ide);
+      }
+      const unsigned at16 = __ballot_sync(kFull, rank == kHalf);
+      const u64 bound_q = at16 ? __shfl_sync(kFull, x.x, __ffs(at16) - 1) : xe.x;
+      __syncwarp();
+      dir.insert(pos++, dd.x, p, 0xFFFFu);
+      dir.insert(pos++, bound_q, q, (1u << (kBucket + 1 - kHalf)) - 1u);
+    }
+    e += k;
+  }
+  c.reserved = h.reserved;
+  c.allocated = h.allocated;
+  c.peak_allocated = h.peak_allocated;
+  c.F = h.F;
+  c.maxF = h.maxF;
+  __syncwarp();
+  if (lane == 0) {
+    ws->peak_reserved = h.peak_reserved;
+    ws->next_base = h.next_base;
+    ws->nseg = h.nseg;
+    ws->nseg_peak = h.nseg_peak;
+  }
+  __syncwarp();
+  wm = h.wm;
+  abase = h.abase;
+  return h.r;
+}
+
 // ---- one trace ---------------------------------------------------------------
 
 template <class D>
@@ -765,7 +965,7 @@ __device__ __forceinline__ void replay_trace(
     pm_result_t* __restrict__ results, int64_t* __restrict__ timeline,
     u32* rec_base, const NPool& P, D& dir, NStage& sg, int lane,
     const u64* __restrict__ wire, pm_req_t* __restrict__ expand,
-    bool expand_overflow, int long_trace) {
+    bool expand_overflow, int long_trace, const NCk& ck) {
   const long long e0 = offs[tr];
   const int n = (int)(offs[tr + 1] - e0);  // < 2^31 (pm_replay_batch)
   const pm_cfg_t* cp = cfgs + (cfg_of ? cfg_of[tr] : 0);
@@ -832,7 +1032,8 @@ __device__ __forceinline__ void replay_trace(
   // request) in every pass, and long traces are the ones that outgrow the
   // earlier passes' capacity and restart: send it straight to the last
   // narrow pass.
-  const bool skip = n >= long_trace;
+  const bool resumed = D::kResumes && ck.load && ck.off[tr] >= 0;
+  const bool skip = !resumed && n >= long_trace;
 
   // requests arrive as pm_req_t (16 B) or as wire words (8 B, decoded in
   // shared memory below)
@@ -845,6 +1046,14 @@ __device__ __forceinline__ void replay_trace(
     status = PM_POOL_OVERFLOW;
     stop = 0;
   }
+  int r0 = 0;  // first request to replay (a checkpoint's resume point)
+  if constexpr (D::kResumes) {
+    if (resumed) r0 = resume_state(ck, tr, c, ws, P, dir, rec, wm, abase, lane);
+  }
+  __syncwarp();
+  // until a checkpoint is saved, the next pass restarts this trace
+  if (ck.save && lane == 0) ck.off[tr] = -1;
+  const int k0 = r0 >> 5;
   auto fetch = [&](int k, u32 buf) {
     const int cnt = min(n - 32 * k, 32);
     if (wire) {
@@ -857,10 +1066,14 @@ __device__ __forceinline__ void replay_trace(
                 sg.bar + buf);
     }
   };
-  if (lane == 0 && nchunks > 0) fetch(0, sg.g & 1);
+  if (lane == 0 && k0 < nchunks) fetch(k0, sg.g & 1);
 
-  for (int k = 0; k < nchunks; ++k) {
+  for (int k = k0; k < nchunks; ++k) {
     const int cbase = 32 * k;
+    if (wire) {
+      __syncwarp();
+      ws->abase_chunk = abase;  // uniform store: a checkpoint's resume point
+    }
     const u32 b = sg.g & 1;
     mbar_wait(sg.bar + b, (sg.g >> 1) & 1);
     if (lane == 0 && k + 1 < nchunks) {
@@ -967,12 +1180,14 @@ __device__ __forceinline__ void replay_trace(
     }
     __syncwarp();
 
-    uint4 ev_next = reinterpret_cast<const uint4*>(cb)[0];
-    for (int j = 0; j < cnt; ++j) {
+    const int j0 = k == k0 ? (r0 & 31) : 0;
+    uint4 ev_next = reinterpret_cast<const uint4*>(cb)[j0];
+    for (int j = j0; j < cnt; ++j) {
       // the next request's word is loaded before this one's dependent chain
       // (slot 32 lies inside the staging area: read, never used)
       const uint4 ev = ev_next;
       ev_next = reinterpret_cast<const uint4*>(cb)[j + 1];
+      bool handoff = false;  // an entry was parked: hand off after this request
       const int hj = (int)ev.y;
       const unsigned kind = ev.z & 3u;
       const int pre = (int)((ev.z >> 2) & 63u);
@@ -1132,6 +1347,7 @@ __device__ __forceinline__ void replay_trace(
               if ((newR || moved) && R != kNone)
                 set_link(rec, st, hcmp, lane, R, 0, kFreeTag | (u32)nid);
               if (split_out) out_R = kFreeTag | (u32)nid;
+              handoff = nid == kStashId;
             }
           }
         }
@@ -1160,7 +1376,7 @@ __device__ __forceinline__ void replay_trace(
         if (pmb::g_inject[1] == 2 && lane == 0 && hj >= 0)
           *rec.word((u32)hj, 2) = (u32)hj;  // a ref that is not mutual
       }
-      if (sts == PM_OK) {
+      if (sts == PM_OK && !handoff) {
         __syncwarp();
         const int code = validate_narrow(P, dir, rec, wm, c, ws, s, lane);
         if (code) {
@@ -1178,6 +1394,20 @@ __device__ __forceinline__ void replay_trace(
         tl[cbase + j] =
             make_longlong2(c.reserved, c.allocated);
       __syncwarp();
+      if (handoff) {
+        // the request is complete; continue at the next one in the next pass
+        status = PM_POOL_OVERFLOW;
+        stop = cbase + j + 1;
+        if (ck.save) {
+          // records of this chunk's handles not seen yet are not state yet:
+          // make them "never allocated" for the next pass
+          const unsigned done_l = j == 31 ? kFull : (2u << j) - 1u;
+          const unsigned same = __match_any_sync(kFull, hcmp);
+          if (fresh && (done_l >> lane & 1u) == 0u && (same & done_l) == 0u)
+            *myrec = make_uint4(0, 0, 0, 0);
+        }
+        break;  // the checkpoint is written after the chunk loop
+      }
     }
     __syncwarp();
     sg.g += 1;
@@ -1191,6 +1421,11 @@ __device__ __forceinline__ void replay_trace(
     }
   }
 
+  if (status == PM_POOL_OVERFLOW && stop > 0 && ck.save) {
+    // handed off after request stop - 1 (a parked entry): leave the state
+    __syncwarp();
+    save_checkpoint(ck, tr, stop, wm, ws->abase_chunk, c, ws, P, dir, lane);
+  }
   if (wire != nullptr &&
       (status == PM_ENCODING_LIMIT ||
        (status == PM_POOL_OVERFLOW && expand_overflow))) {
@@ -1254,9 +1489,13 @@ __device__ __forceinline__ NStage carve_stage(char* wst) {
 //
 // Passes of one pm_replay_batch, in launch order (Ctl work / n_list index):
 //   0 main narrow pass (register directory, CTA-shared pool)
-//   1 narrow, memory directory, entries in shared memory   (kTierMemSmem)
-//   2 narrow, memory directory, entries in HBM              (kTierMemHbm)
-//   3..6 the wide tiers 1-4 of replay_device.cuh            (kTierWide1..)
+//   1 narrow, memory directory, entries in shared memory, several warps
+//     per SM with a private pool each                        (kTierMemSmem)
+//   2 the same with one warp owning the SM's shared memory   (kTierMemSmemBig)
+//   3 narrow, memory directory, entries in HBM              (kTierMemHbm)
+//   4..7 the wide tiers 1-4 of replay_device.cuh            (kTierWide1..)
+// Between narrow passes a trace moves with its checkpoint (NCk) and
+// continues where it stopped.
 // A capacity overflow moves a trace to the next capacity tier; an encoding
 // limit sends it to the first wide tier.
 // requests: a trace this long goes straight to pass 2 when the batch is too
@@ -1264,9 +1503,10 @@ __device__ __forceinline__ NStage carve_stage(char* wst) {
 constexpr int kLongTrace = 1 << 20;
 constexpr int kNoSkip = 0x7FFFFFFF;
 constexpr int kTierMemSmem = 1;
-constexpr int kTierMemHbm = 2;
-constexpr int kTierWide1 = 3;
-constexpr int kTierWide4 = 6;
+constexpr int kTierMemSmemBig = 2;
+constexpr int kTierMemHbm = 3;
+constexpr int kTierWide1 = 4;
+constexpr int kTierWide4 = 7;
 
 __device__ __forceinline__ void route(pmb::Ctl* ctl, int sts, int tr,
                                       int next_pass,
@@ -1284,6 +1524,7 @@ __device__ __forceinline__ void route(pmb::Ctl* ctl, int sts, int tr,
 // positions by physical bucket, a stack of free physical buckets.  Same
 // interface as NDir; find is a 32-ary warp search over the sorted bounds.
 struct NDirMem {
+  static constexpr bool kResumes = true;  // passes 1-3 continue checkpoints
   u64* db;          // [nbmax] bound by position
   int* dp;          // [nbmax] physical bucket by position
   unsigned* m;      // [nbmax] occupancy mask by position
@@ -1473,10 +1714,19 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
                          int n_groups, const volatile unsigned* ready,
                          const u64* __restrict__ wire,
                          pm_req_t* __restrict__ expand,
-                         int32_t* __restrict__ enc_list, int long_trace) {
+                         int32_t* __restrict__ enc_list, int long_trace,
+                         long long* __restrict__ ck_off, char* __restrict__ ck_base,
+                         unsigned long long ck_cap) {
   extern __shared__ __align__(16) char smem[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
+  NCk ck;
+  ck.off = ck_off;
+  ck.base = ck_base;
+  ck.used = &ctl->ck_used;
+  ck.cap = ck_cap;
+  ck.save = ck_off != nullptr;
+  ck.load = false;
   const size_t E = (size_t)buckets * kBucket;
   NPool P;
   P.ka = reinterpret_cast<u64*>(smem);
@@ -1513,7 +1763,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
     const int tr = list ? list[t] : (int)t;
     if (lane == 0) atomicAdd(active, 1);
     replay_trace(tr, reqs, offs, cfgs, cfg_of, results, timeline, recs, P, dir,
-                 sg, lane, wire, expand, false, long_trace);
+                 sg, lane, wire, expand, false, long_trace, ck);
     __syncwarp();
     if (lane == 0) atomicSub(active, 1);
     const int sts = results[tr].status;
@@ -1527,7 +1777,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
 // CTA pool, with the directory in shared memory and the entries in shared
 // memory (SMEM_POOL) or in a per-CTA HBM region.
 template <bool SMEM_POOL>
-__global__ void __launch_bounds__(32, 1)
+__global__ void __launch_bounds__(256, 1)
     replay_narrow_mem_kernel(const pm_req_t* __restrict__ reqs,
                              const int64_t* __restrict__ offs,
                              const pm_cfg_t* __restrict__ cfgs,
@@ -1540,11 +1790,25 @@ __global__ void __launch_bounds__(32, 1)
                              int32_t* __restrict__ enc_list,
                              char* __restrict__ gpool, int nbmax,
                              const u64* __restrict__ wire,
-                             pm_req_t* __restrict__ expand, int long_trace) {
+                             pm_req_t* __restrict__ expand, int long_trace,
+                             long long* __restrict__ ck_off, char* __restrict__ ck_base,
+                             unsigned long long ck_cap, size_t warp_bytes) {
   extern __shared__ __align__(16) char smem[];
   const int lane = threadIdx.x & 31;
-  NStage sg = carve_stage(smem);
-  char* dbase = smem + kWarpStageBytes;
+  // each warp of the CTA owns a slice of the shared memory (its staging,
+  // directory and, in the shared-memory passes, its bucket pool)
+  char* wsm = smem + (size_t)(threadIdx.x >> 5) * warp_bytes;
+  NStage sg = carve_stage(wsm);
+  NCk ck;
+  ck.off = ck_off;
+  ck.base = ck_base;
+  ck.used = &ctl->ck_used;
+  ck.cap = ck_cap;
+  // pass 1 checkpoints for pass 2; pass 2 hands off to the wide tiers,
+  // which replay from the start in their own representation
+  ck.save = SMEM_POOL && ck_off != nullptr;
+  ck.load = ck_off != nullptr;
+  char* dbase = wsm + kWarpStageBytes;
   NDirMem dir;
   dir.nbmax = nbmax;
   dir.db = reinterpret_cast<u64*>(dbase);
@@ -1573,10 +1837,11 @@ __global__ void __launch_bounds__(32, 1)
     // the last narrow tier expands wire words for the wide tier it hands to
     replay_trace(tr, reqs, offs, cfgs, cfg_of, results, timeline, recs, P, dir,
                  sg, lane, wire, expand, !SMEM_POOL,
-                 SMEM_POOL ? long_trace : kNoSkip);
+                 SMEM_POOL ? long_trace : kNoSkip, ck);
     __syncwarp();
     if (lane == 0)
-      route(ctl, results[tr].status, tr, SMEM_POOL ? kTierMemHbm : kTierWide4,
+      route(ctl, results[tr].status, tr,
+            !SMEM_POOL ? kTierWide4 : pass == kTierMemSmem ? kTierMemSmemBig : kTierMemHbm,
             overflow_list, enc_list);
   }
 }

@@ -82,9 +82,9 @@ class DeviceBatch:
     def tier_counts(self) -> list[int]:
         """Traces the last launch handed to each retry pass (diagnostic: the
         workspace's control block, csrc/replay_device.cuh Ctl): narrow
-        memory-directory passes 1-2, then wide tiers 1-4."""
+        memory-directory passes 1-3, then wide tiers 1-4."""
         ctl = self.d_ws[:64].cpu().numpy().view(np.uint32)
-        return [int(x) for x in ctl[9:15]]
+        return [int(x) for x in ctl[9:16]]
 
     def results(self) -> np.ndarray:
         self.torch.cuda.synchronize(self.device)

@@ -103,3 +103,31 @@ def test_c5_style_trace_vs_oracle():
     got = api.build_sequence(api.analyze(b), iterations=2)
     assert [(r.kind.value, r.block_id, r.size, r.virtual_ts)
             for r in got.requests] == want
+
+
+def test_c5_1e6_events_vs_oracle():
+    """GPU-vs-oracle pipeline parity at 10^6 events (one long
+    C5-style trace, 2 iterations): the orchestrated request sequence and its
+    replay (every result field) equal the CPU oracle's."""
+    import numpy as np
+    from oracle import pipeline as op
+    from oracle import replay as oracle_replay
+    from paper_2504_03887_b200 import synth_events
+    from paper_2504_03887_b200.allocator import AllocatorConfig, cfg_record
+    from paper_2504_03887_b200.estimator import replay_sequence
+    b = synth_events.generate(36000, iterations=2)
+    assert len(b) > 1_000_000
+    recs = b.to_json_dict()["traceEvents"]
+    side = {"param_sizes": list(b.metadata.param_sizes),
+            "batch_bytes": list(b.metadata.batch_bytes)}
+    want = op.build_sequence(op.normalize(recs), side, 2)
+    got = api.build_sequence(api.analyze(b), iterations=2)
+    assert [(r.kind.value, r.block_id, r.size, r.virtual_ts)
+            for r in got.requests] == want
+    res = replay_sequence(got, AllocatorConfig(), timeline=False)
+    offs = np.array([0, len(got.packed)], dtype=np.int64)
+    ref, _ = oracle_replay.replay_batch(got.packed, offs, cfg_record(AllocatorConfig()))
+    assert res.peak_reserved == int(ref[0]["peak_reserved"])
+    assert res.peak_allocated == int(ref[0]["peak_allocated"])
+    assert res.final_reserved == int(ref[0]["final_reserved"])
+    assert res.n_segments_peak == int(ref[0]["n_segments_peak"])

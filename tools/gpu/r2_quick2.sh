@@ -1,0 +1,5 @@
+set -x
+python -c "import __graft_entry__ as g; g.build()" 2>&1 | tail -2
+timeout 900 python -m pytest -x -q -m gpu tests/test_replay_gpu.py tests/test_replay_narrow_gpu.py tests/test_config_goldens.py 2>&1 | tail -2
+for i in 1 2; do timeout 300 python tools/prof_replay.py --traces 10000 --launches 3 2>&1 | tail -1; done
+timeout 900 python tools/bench_frag.py 2>&1 | tail -1

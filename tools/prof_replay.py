@@ -37,7 +37,7 @@ def main():
         res = batch.results()
         ev = int(res["n_events_replayed"].sum())
         ctl = batch.d_ws[:64].cpu().numpy().view(np.uint32)
-        print(f"retries: narrow passes {ctl[9:11].tolist()}, wide tiers {ctl[11:15].tolist()}")
+        print(f"retries: narrow passes {ctl[9:12].tolist()}, wide tiers {ctl[12:16].tolist()}")
         print(f"{args.traces} traces {ev} events {dt*1e3:.1f} ms "
               f"{ev/dt/1e9:.3f} Gev/s maxF {res['max_free_blocks'].max()} "
               f"status {set(res['status'].tolist())}")
