@@ -190,6 +190,7 @@ struct NDir {
   }
   __device__ __forceinline__ int alloc_phys() {
     int p = -1;
+    PM_STAT(12);
     if (lane == 0) {
       for (int w = 0; w < cta_words && p < 0; ++w) {
         unsigned v = *(volatile unsigned*)&cta_used[w];
@@ -221,6 +222,7 @@ struct NDir {
     int* ctr = reinterpret_cast<int*>(cta_used + cta_words);
     if (lane == 0) atomicAdd(&ctr[0], 1);
     for (;;) {
+      PM_STAT(13);
       __nanosleep(500);
       p = alloc_phys();
       if (p >= 0) break;
@@ -1245,6 +1247,7 @@ __device__ __forceinline__ void replay_trace(
               }
             } else {
               // miss: new segment (allocator.py:278-288, 244-250)
+              PM_STAT(14);
               pmb::Cfg wc;
               wc.cp = ws->cp;
               const long long seg =
@@ -1296,6 +1299,7 @@ __device__ __forceinline__ void replay_trace(
             const bool lf = is_free_ref(L), rf = is_free_ref(R);
             up = true;
             if (!lf && !rf) {
+              PM_STAT(15);
               up_ka = pk(S, A);
               up_l = pmb::mk_links(L, R);
             } else if (lf && !rf) {

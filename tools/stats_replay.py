@@ -14,7 +14,8 @@ REPO = Path(__file__).resolve().parent.parent
 sys.path.insert(0, str(REPO))
 NAMES = ["rekey in place", "rekey moved", "remove", "remove fill-hole", "bucket erase",
          "insert", "split", "merge", "best-fit scan", "best-fit next bucket",
-         "argmin multi-candidate", "argmin key tie"]
+         "argmin multi-candidate", "argmin key tie", "bucket alloc (bitmap)",
+         "bucket wait round", "alloc miss (segment)", "free, no free neighbour"]
 
 
 def main():
