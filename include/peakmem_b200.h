@@ -129,7 +129,9 @@ typedef enum {
   PM_ERR_CUDA = 2,
   PM_ERR_WORKSPACE_TOO_SMALL = 3,
   PM_ERR_NO_DEVICE = 4,
-  PM_ERR_CYCLIC_PARENT = 5   /* pm_layer_tree: -> CyclicParentLink */
+  PM_ERR_CYCLIC_PARENT = 5,  /* pm_layer_tree: -> CyclicParentLink */
+  PM_ERR_ENGINE_LIMIT = 6,   /* a packed key range exceeded: -> EngineLimitExceeded */
+  PM_ERR_SKIPPED = 7         /* pm_pipeline_batch: the caller skipped the trace */
 } pm_err_t;
 
 const char* pm_last_error(void);

@@ -21,6 +21,9 @@
  *                     emission and total order (orchestration.py:270-387)
  *   pm_layer_tree  -> analysis.build_layer_tree's ancestor walk, child
  *                     order and walk order (analysis.py:113-182)
+ *   pm_pipeline_batch -> orchestration.analyze + orchestration.build_sequence
+ *                     (orchestration.py:107-116, 237-399) for B traces in one
+ *                     call, device columns in, the replay batch out
  */
 #ifndef PEAKMEM_PIPELINE_H
 #define PEAKMEM_PIPELINE_H
@@ -98,6 +101,77 @@ int pm_layer_tree(int64_t n, const int64_t* pid, const int64_t* par,
                   int64_t* node_parent,
                   int64_t* child_order, int64_t* child_off, int64_t* walk,
                   int64_t* n_walk, void* stream);
+
+
+/* ---- the batched, device-resident pipeline ------------------------------
+ *
+ * pm_pipeline_batch -> orchestration.analyze (orchestration.py:107-116) then
+ * orchestration.build_sequence (orchestration.py:237-399) for n_traces
+ * traces at once, as PeakMemoryEstimator.estimate calls them
+ * (estimator.py:146,152).  The event columns of all traces are concatenated
+ * trace-major (each trace in event order, i.e. the order parse_trace sorts
+ * into) and passed as DEVICE pointers with HOST per-trace offsets; the
+ * per-trace orchestration parameters (a handful of values derived from the
+ * trace's markers and sidecar on the host, exactly as build_sequence
+ * derives them) are HOST arrays in CSR form.  The orchestrated requests of
+ * all traces are written to `reqs` (DEVICE, capacity req_cap) in the layout
+ * pm_replay_batch reads: trace t is reqs[req_off[t] .. req_off[t+1]) with
+ * dense per-trace handles, so the replay runs on it without a host round
+ * trip.  Timestamps are integer microseconds; INT64_MIN = None. */
+typedef struct {
+  int32_t n_traces;
+  /* host offsets [n_traces + 1] into the three event columns */
+  const int64_t* fn_off;  /* python_function frames */
+  const int64_t* op_off;  /* cpu_op events */
+  const int64_t* in_off;  /* cpu_instant_event events */
+  /* device columns */
+  const int64_t* fn_pid;        /* python id (INT64_MIN = None) */
+  const int64_t* fn_par;        /* parent python id (INT64_MIN = None) */
+  const uint8_t* fn_is_layer;   /* name starts with a layer prefix */
+  const int64_t* fn_start;
+  const int64_t* fn_end;
+  const int64_t* op_start;
+  const int64_t* op_end;
+  const int64_t* op_seq;        /* sequence number, -1 = None */
+  const int64_t* in_start;
+  const int64_t* in_addr;
+  const int64_t* in_nbytes;
+  /* host, per trace (CSR offsets [n_traces + 1]) -- see build_sequence */
+  const int64_t* span_off;      /* optimizer-step markers in marker order */
+  const int64_t* span_start;
+  const int64_t* span_end;
+  const int64_t* span_iter;
+  const int64_t* param_off;     /* sidecar param sizes, sorted unique */
+  const int64_t* param_sizes;
+  const int64_t* win_off;       /* windows of the included iterations */
+  const int64_t* win_start;
+  const int64_t* win_end;
+  const int64_t* zg_off;        /* zero-grad starts incl. cloned markers, sorted */
+  const int64_t* zg;
+  const int32_t* clones;        /* [n_traces] iterations cloned */
+  const int64_t* tpl_start;     /* [n_traces] clone template window */
+  const int64_t* tpl_end;
+  const int64_t* shift;         /* [n_traces] template width */
+  const int64_t* bat_off;       /* batch requests (vts, size, kind, it, j) */
+  const int64_t* bat_vts;
+  const int64_t* bat_size;
+  const int32_t* bat_kind;
+  const int64_t* bat_it;
+  const int64_t* bat_j;
+  const int32_t* skip;          /* [n_traces] nullable: nonzero = emit nothing
+                                   (a trace that failed a host-side check) */
+} pm_pipeline_batch_t;
+
+/* Returns 0 or a pm_err_t (PM_ERR_WORKSPACE_TOO_SMALL: req_cap is below
+ * req_off[n_traces], which is filled in; PM_ERR_ENGINE_LIMIT: a packed key
+ * range exceeded).  Per trace (host outputs): req_off [n_traces + 1],
+ * status (0; -1 NoGradientBlocks; PM_ERR_CYCLIC_PARENT; PM_ERR_SKIPPED),
+ * n_model (model-load requests), breakdown (nullable, [n_traces x 8]:
+ * ALLOC bytes by role code 0 unclassified, 1 model, 2 batch, 3 gradient,
+ * 4 optimizer_state, 5 temporary, 6 retained -- estimator.py:160-164). */
+int pm_pipeline_batch(const pm_pipeline_batch_t* in, pm_req_t* reqs,
+                      int64_t req_cap, int64_t* req_off, int32_t* status,
+                      int64_t* n_model, int64_t* breakdown, void* stream);
 
 #ifdef __cplusplus
 }

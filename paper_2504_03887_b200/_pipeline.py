@@ -14,8 +14,12 @@ from .errors import EngineLimitExceeded, EngineUnavailable
 
 LIB_PATH = LIB_DIR / "libpeakmem_pipeline.so"
 EXPORTED_SYMBOLS = ("pm_pipeline_last_error", "pm_sort_events", "pm_link",
-                    "pm_link_roots", "pm_orchestrate", "pm_layer_tree")
+                    "pm_link_roots", "pm_orchestrate", "pm_layer_tree",
+                    "pm_pipeline_batch")
+PM_ERR_WORKSPACE_TOO_SMALL = 3
 PM_ERR_CYCLIC_PARENT = 5
+PM_ERR_ENGINE_LIMIT = 6
+PM_ERR_SKIPPED = 7
 NONE = np.iinfo(np.int64).min
 
 _lib = None
@@ -45,6 +49,8 @@ def _i64(a):
 
 
 def _check(rc: int, lib) -> None:
+    if rc == PM_ERR_ENGINE_LIMIT:
+        raise EngineLimitExceeded(lib.pm_pipeline_last_error().decode(errors="replace"))
     if rc != 0:
         msg = lib.pm_pipeline_last_error().decode(errors="replace")
         raise RuntimeError(f"peakmem_b200 pipeline error {rc}: {msg}")
@@ -271,3 +277,45 @@ def orchestrate(b_alloc, b_size, b_free, b_role, spans, param_sizes, windows,
             setattr(o, f, getattr(o, f)[:n])
     o.fb_role, o.fb_free, o.fb_flags = o.fb_role[:nb], o.fb_free[:nb], o.fb_flags[:nb]
     return o
+
+
+# ---- the batched, device-resident pipeline (pm_pipeline_batch) -------------
+
+_BATCH_FIELDS = [
+    ("n_traces", ctypes.c_int32),
+    *[(f, ctypes.c_void_p) for f in (
+        "fn_off", "op_off", "in_off",
+        "fn_pid", "fn_par", "fn_is_layer", "fn_start", "fn_end",
+        "op_start", "op_end", "op_seq", "in_start", "in_addr", "in_nbytes",
+        "span_off", "span_start", "span_end", "span_iter", "param_off",
+        "param_sizes", "win_off", "win_start", "win_end", "zg_off", "zg",
+        "clones", "tpl_start", "tpl_end", "shift", "bat_off", "bat_vts",
+        "bat_size", "bat_kind", "bat_it", "bat_j", "skip")],
+]
+
+
+class PipelineBatch(ctypes.Structure):
+    """pm_pipeline_batch_t (include/peakmem_pipeline.h)."""
+
+    _fields_ = _BATCH_FIELDS
+
+
+def pipeline_batch(desc: PipelineBatch, d_reqs_ptr: int, req_cap: int,
+                   n_traces: int):
+    """Run pm_pipeline_batch; the host arrays `desc` points at must stay
+    alive for the call.  Returns (req_off, status, n_model, breakdown)."""
+    lib = load()
+    _native.require_device()
+    req_off = np.zeros(n_traces + 1, np.int64)
+    status = np.zeros(n_traces, np.int32)
+    n_model = np.zeros(n_traces, np.int64)
+    breakdown = np.zeros((n_traces, 8), np.int64)
+    rc = lib.pm_pipeline_batch(ctypes.byref(desc), ctypes.c_void_p(d_reqs_ptr),
+                               ctypes.c_int64(req_cap), _p(req_off), _p(status),
+                               _p(n_model), _p(breakdown),
+                               ctypes.c_void_p(_stream()))
+    if rc == PM_ERR_WORKSPACE_TOO_SMALL:
+        raise MemoryError(f"pm_pipeline_batch: {int(req_off[-1])} requests > "
+                          f"capacity {req_cap}")
+    _check(rc, lib)
+    return req_off, status, n_model, breakdown

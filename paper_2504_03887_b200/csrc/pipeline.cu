@@ -204,7 +204,8 @@ __global__ void k_layer_anc(const long long* lay, long long nl,
                             const long long* pid, const long long* parent_pos,
                             const unsigned char* is_layer,
                             const long long* lay_index, long long n,
-                            long long* node_parent, int* cyclic) {
+                            const int* tr, long long* node_parent,
+                            int* cyclic) {
   long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (v >= nl) return;
   const long long e = lay[v];
@@ -214,7 +215,7 @@ __global__ void k_layer_anc(const long long* lay, long long nl,
   long long anc = -1;
   while (c >= 0) {
     if (c == e || (own != kNoneTs && pid[c] == own) || ++steps > n) {
-      atomicExch(cyclic, 1);
+      atomicExch(&cyclic[tr ? tr[e] : 0], 1);
       anc = -1;
       break;
     }
@@ -374,14 +375,18 @@ __global__ void k_addr_keys(const long long* addr, long long n, u64* keys,
 
 // free_time of a positive instant = ts of the next instant at its address
 // in (ts, event_id) order (analysis.py:265-290)
+// (batched: tr = trace of each instant; an address recurs only within its
+// own trace -- the stable sort keeps each trace's run of an address together)
 __global__ void k_next_same_addr(const u64* skeys, const long long* sidx,
                                  long long n, const long long* start,
-                                 long long* free_time) {
+                                 const int* tr, long long* free_time) {
   long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (i >= n) return;
   const long long k = sidx[i];
   long long ft = kNoneTs;
-  if (i + 1 < n && skeys[i + 1] == skeys[i]) ft = start[sidx[i + 1]];
+  if (i + 1 < n && skeys[i + 1] == skeys[i] &&
+      (tr == nullptr || tr[sidx[i + 1]] == tr[k]))
+    ft = start[sidx[i + 1]];
   free_time[k] = ft;
 }
 
@@ -946,8 +951,8 @@ int sort_pairs(Arena& A, u64* keys, long long* vals, long long n, int end_bit = 
   return PM_SUCCESS;
 }
 
-template <class T>
-int excl_sum(Arena& A, const T* in, T* out, long long n) {
+template <class T, class U>
+int excl_sum(Arena& A, const T* in, U* out, long long n) {
   if (n <= 0) return PM_SUCCESS;
   size_t tmp = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, tmp, in, out, (int64_t)n, A.s);
@@ -1151,7 +1156,8 @@ int stage_roots(Arena& A, long long no, const long long* d_ostart,
 
 // a7 (analysis.py:252-294)
 int stage_group(Arena& A, long long ni, const long long* d_istart,
-                const long long* d_iaddr, const long long* d_inb, BlocksDev* B) {
+                const long long* d_iaddr, const long long* d_inb, BlocksDev* B,
+                const int* d_itr = nullptr) {
   cudaStream_t s = A.s;
   u64* akeys = A.alloc<u64>(ni);
   long long* aidx = A.alloc<long long>(ni);
@@ -1167,7 +1173,8 @@ int stage_group(Arena& A, long long ni, const long long* d_istart,
   if (ni > 0) {
     k_addr_keys<<<blocks_for(ni), 256, 0, s>>>(d_iaddr, ni, akeys, aidx);
     PM_TRY(sort_pairs(A, akeys, aidx, ni));
-    k_next_same_addr<<<blocks_for(ni), 256, 0, s>>>(akeys, aidx, ni, d_istart, free_inst);
+    k_next_same_addr<<<blocks_for(ni), 256, 0, s>>>(akeys, aidx, ni, d_istart, d_itr,
+                                                    free_inst);
     k_positive<<<blocks_for(ni), 256, 0, s>>>(d_inb, ni, pos);
     PM_TRY(excl_sum(A, pos, pexcl, ni));
     nb = read_scalar(pexcl + ni - 1, s) + read_scalar(pos + ni - 1, s);
@@ -1477,374 +1484,8 @@ int pm_link_roots(int64_t n_roots, const int64_t* root_start,
   return sync_check(s, "pm_link_roots");
 }
 
-// a13-a19 (orchestration.py:237-399) after link.  Inputs (host):
-//   blocks (block-id order): alloc, size, free (INT64_MIN = None), role
-//     (3 marks the blocks tag_gradient_blocks tagged);
-//   spans: optimizer-step markers in marker order (start, end, iteration);
-//   param_sizes sorted unique; windows (start, end) of the included
-//   iterations; zero-grad starts sorted (original + cloned markers);
-//   clones, template window, shift (template width);
-//   batch requests already built on the host (tiny): n_batch records of
-//   (vts, size, kind, iteration, j).
-// Outputs (host, capacity req_cap >= n_model + n_batch + 2 * blocks *
-// (1 + clones)): the ordered sequence -- raw index, kind, size, vts, tag
-// (0 model / 1 batch / 2 block / 3 clone), a, b, role -- the packed replay
-// records, per-block final role / free / flags, n_model.  Status -1 in
-// *n_req_out means NoGradientBlocks.
-int pm_orchestrate(int64_t nb, const int64_t* b_alloc, const int64_t* b_size,
-                   const int64_t* b_free, const int32_t* b_role, int32_t n_spans,
-                   const int64_t* span_start, const int64_t* span_end,
-                   const int64_t* span_iter, int32_t n_param,
-                   const int64_t* param_sizes, int32_t n_windows,
-                   const int64_t* win_start, const int64_t* win_end,
-                   int32_t n_zg, const int64_t* zg, int32_t clones,
-                   int64_t tpl_start, int64_t tpl_end, int64_t shift,
-                   int64_t n_batch, const int64_t* batch_vts,
-                   const int64_t* batch_size, const int32_t* batch_kind,
-                   const int64_t* batch_it, const int64_t* batch_j,
-                   int64_t req_cap, int64_t* n_req_out, int64_t* n_model_out,
-                   int64_t* o_raw, int32_t* o_kind, int64_t* o_size,
-                   int64_t* o_vts, int32_t* o_tag, int64_t* o_a, int64_t* o_b,
-                   int32_t* o_role, pm_req_t* o_packed, int32_t* fb_role,
-                   int64_t* fb_free, int32_t* fb_flags, void* stream_) {
-  using namespace pmp;
-  cudaStream_t s = (cudaStream_t)stream_;
-  Arena A(s);
-  OrchParams p;
-  p.n_spans = n_spans;
-  p.span_start = A.upload((const long long*)span_start, n_spans);
-  p.span_end = A.upload((const long long*)span_end, n_spans);
-  p.span_iter = A.upload((const long long*)span_iter, n_spans);
-  p.n_param = n_param;
-  p.param_sizes = A.upload((const long long*)param_sizes, n_param);
-  p.n_windows = n_windows;
-  p.win_start = A.upload((const long long*)win_start, n_windows);
-  p.win_end = A.upload((const long long*)win_end, n_windows);
-  p.n_zg = n_zg;
-  p.zg = A.upload((const long long*)zg, n_zg);
-  p.tpl_start = tpl_start;
-  p.tpl_end = tpl_end;
-  p.clones = clones;
-  p.shift = shift;
-  long long* d_alloc = A.upload((const long long*)b_alloc, nb);
-  long long* d_size = A.upload((const long long*)b_size, nb);
-  long long* d_free = A.upload((const long long*)b_free, nb);
-  int* d_role_in = A.upload((const int*)b_role, nb);
-  int* d_grad = A.alloc<int>(nb);
-  int* d_role = A.alloc<int>(nb);
-  long long* d_free0 = A.alloc<long long>(nb);
-  long long* d_freeo = A.alloc<long long>(nb);
-  int* d_flags = A.alloc<int>(nb);
-  if (A.err != cudaSuccess) return perr(PM_ERR_CUDA, "pm_orchestrate: alloc");
-  // gradient tags are the role-3 blocks of link
-  {
-    std::vector<int> g(nb);
-    for (long long i = 0; i < nb; ++i) g[i] = b_role[i] == R_GRAD ? 1 : 0;
-    if (nb) cudaMemcpyAsync(d_grad, g.data(), sizeof(int) * nb, cudaMemcpyHostToDevice, s);
-    cudaStreamSynchronize(s);
-  }
-  if (nb > 0)
-    k_orch_blocks<<<blocks_for(nb), 256, 0, s>>>(p, d_alloc, d_size, d_free, d_role_in, d_grad,
-                                                 nb, d_role, d_free0, d_freeo, d_flags);
-  int rc = download(fb_role, (const int32_t*)d_role, nb, s);
-  if (!rc) rc = download(fb_free, (const int64_t*)d_freeo, nb, s);
-  if (!rc) rc = download(fb_flags, (const int32_t*)d_flags, nb, s);
-  if (rc) return rc;
-  rc = sync_check(s, "pm_orchestrate blocks");
-  if (rc) return rc;
-  // counts: model, chosen (1 or 2 requests each), template (per clone)
-  long long n_model = 0;
-  std::vector<long long> chosen_off(nb), tpl_off(nb), model_sizes;
-  long long n_chosen_req = 0, n_tpl_req = 0;
-  for (long long b = 0; b < nb; ++b) {
-    const int f = fb_flags[b];
-    if (f & F_MODEL) model_sizes.push_back(b_size[b]);
-    chosen_off[b] = n_chosen_req;
-    if (f & F_CHOSEN) n_chosen_req += fb_free[b] != kNoneTs ? 2 : 1;
-    tpl_off[b] = n_tpl_req;
-    if (f & F_TPL) n_tpl_req += 2;  // absent clone frees compacted later
-  }
-  n_model = (long long)model_sizes.size();
-  *n_model_out = n_model;
-  if (n_model == 0) {
-    *n_req_out = -1;  // NoGradientBlocks (orchestration.py:152-153)
-    return PM_SUCCESS;
-  }
-  // clone slots are reserved 2 per template block; absent frees are
-  // compacted out after emission
-  const long long base_batch = n_model;
-  const long long base_chosen = base_batch + n_batch;
-  const long long base_clone = base_chosen + n_chosen_req;
-  const long long n_raw_max = base_clone + (long long)clones * n_tpl_req;
-  if (n_raw_max > req_cap) return perr(PM_ERR_WORKSPACE_TOO_SMALL, "pm_orchestrate: req_cap");
-  std::vector<RawReq> head(base_chosen);
-  for (long long i = 0; i < n_model; ++i) {
-    RawReq r{};
-    r.vts = i - n_model;
-    r.size = model_sizes[n_model - 1 - i];  // reversed backward order
-    r.a = i;
-    r.kind = 0;
-    r.tag = 0;
-    r.role = R_MODEL;
-    head[i] = r;
-  }
-  for (long long i = 0; i < n_batch; ++i) {
-    RawReq r{};
-    r.vts = batch_vts[i];
-    r.size = batch_size[i];
-    r.a = batch_it[i];
-    r.b = batch_j[i];
-    r.kind = batch_kind[i];
-    r.tag = 1;
-    r.role = R_BATCH;
-    head[base_batch + i] = r;
-  }
-  RawReq* raw = A.alloc<RawReq>(n_raw_max);
-  long long* d_coff = A.upload(chosen_off.data(), nb);
-  long long* d_toff = A.upload(tpl_off.data(), nb);
-  if (A.err != cudaSuccess) return perr(PM_ERR_CUDA, "pm_orchestrate: alloc");
-  // clone slots start as "absent" markers (kind -1)
-  std::vector<RawReq> blank(n_raw_max - base_clone);
-  for (auto& r : blank) r.kind = -1;
-  if (!blank.empty())
-    cudaMemcpyAsync(raw + base_clone, blank.data(), sizeof(RawReq) * blank.size(),
-                    cudaMemcpyHostToDevice, s);
-  cudaMemcpyAsync(raw, head.data(), sizeof(RawReq) * base_chosen, cudaMemcpyHostToDevice, s);
-  if (nb > 0) {
-    k_emit_blocks<<<blocks_for(nb), 256, 0, s>>>(d_flags, d_alloc, d_size, d_freeo, d_role, d_coff,
-                                                 nb, base_chosen, raw);
-    if (clones > 0)
-      k_emit_clones<<<blocks_for(nb), 256, 0, s>>>(d_flags, d_alloc, d_size, d_free0, d_role,
-                                                   d_toff, n_tpl_req, nb, base_clone, p, raw);
-  }
-  rc = sync_check(s, "pm_orchestrate emit");
-  if (rc) return rc;
-  // compact absent clone frees (keeps raw order)
-  long long n_raw = n_raw_max;
-  RawReq* rawc = raw;
-  if (clones > 0 && n_tpl_req > 0) {
-    std::vector<RawReq> h(n_raw_max);
-    cudaMemcpy(h.data(), raw, sizeof(RawReq) * n_raw_max, cudaMemcpyDeviceToHost);
-    long long w = base_clone;
-    for (long long i = base_clone; i < n_raw_max; ++i)
-      if (h[i].kind >= 0) h[w++] = h[i];
-    n_raw = w;
-    rawc = A.alloc<RawReq>(n_raw);
-    cudaMemcpyAsync(rawc, h.data(), sizeof(RawReq) * n_raw, cudaMemcpyHostToDevice, s);
-  }
-  // total order
-  long long* mm = A.alloc<long long>(2);
-  u64* keys = A.alloc<u64>(n_raw);
-  long long* perm = A.alloc<long long>(n_raw);
-  pm_req_t* d_packed = A.alloc<pm_req_t>(n_raw);
-  long long* d_oraw = A.alloc<long long>(n_raw);
-  if (A.err != cudaSuccess) return perr(PM_ERR_CUDA, "pm_orchestrate: alloc");
-  long long init[2] = {INT64_MAX, INT64_MIN};
-  cudaMemcpyAsync(mm, init, sizeof(init), cudaMemcpyHostToDevice, s);
-  k_minmax_vts<<<blocks_for(n_raw), 256, 0, s>>>(rawc, n_raw, mm);
-  long long hmm[2];
-  cudaMemcpyAsync(hmm, mm, sizeof(hmm), cudaMemcpyDeviceToHost, s);
-  rc = sync_check(s, "pm_orchestrate minmax");
-  if (rc) return rc;
-  if ((u64)(hmm[1] - hmm[0]) >= (1ull << 61))
-    return perr(PM_ERR_INVALID_ARGUMENT, "pm_orchestrate: timestamp range too wide");
-  k_order_keys<<<blocks_for(n_raw), 256, 0, s>>>(rawc, n_raw, hmm[0], keys, perm);
-  if (sort_pairs(A, keys, perm, n_raw)) return PM_ERR_CUDA;
-  k_pack<<<blocks_for(n_raw), 256, 0, s>>>(rawc, perm, n_raw, d_packed, d_oraw);
-  std::vector<RawReq> hraw(n_raw);
-  cudaMemcpyAsync(hraw.data(), rawc, sizeof(RawReq) * n_raw, cudaMemcpyDeviceToHost, s);
-  rc = download(o_raw, (const int64_t*)d_oraw, n_raw, s);
-  if (!rc) rc = download(o_packed, (const pm_req_t*)d_packed, n_raw, s);
-  if (rc) return rc;
-  rc = sync_check(s, "pm_orchestrate order");
-  if (rc) return rc;
-  for (long long i = 0; i < n_raw; ++i) {
-    const RawReq& r = hraw[o_raw[i]];
-    o_kind[i] = r.kind;
-    o_size[i] = r.size;
-    o_vts[i] = r.vts;
-    o_tag[i] = r.tag;
-    o_a[i] = r.a;
-    o_b[i] = r.b;
-    o_role[i] = r.role;
-  }
-  *n_req_out = n_raw;
-  return PM_SUCCESS;
-}
-
-// ---- a4 / f4: the layer tree on the device ----------------------------------
-
-int pm_layer_tree(int64_t n, const int64_t* pid, const int64_t* par,
-                  const uint8_t* is_layer, const int64_t* start,
-                  const int64_t* event_id, int64_t n_layers,
-                  int64_t* node_parent,
-                  int64_t* child_order, int64_t* child_off, int64_t* walk,
-                  int64_t* n_walk, void* stream_) {
-  if (n < 0 || n_layers < 0 || n_layers > n ||
-      (n > 0 && (!pid || !par || !is_layer || !start)) ||
-      (n_layers > 0 && (!node_parent || !child_order || !child_off || !walk)))
-    return perr(PM_ERR_INVALID_ARGUMENT, "pm_layer_tree: bad arguments");
-  if (child_off) {
-    child_off[0] = 0;
-    if (n_layers == 0) child_off[1] = 0;
-  }
-  if (n_walk) *n_walk = 0;
-  if (n_layers == 0) return PM_SUCCESS;
-  cudaStream_t s = (cudaStream_t)stream_;
-  const long long nl = n_layers;
-  Arena A(s);
-  const long long* d_pid = (const long long*)A.upload(pid, n);
-  const long long* d_par = (const long long*)A.upload(par, n);
-  const unsigned char* d_isl = A.upload(is_layer, n);
-  const long long* d_start = (const long long*)A.upload(start, n);
-  // python id -> first frame
-  u64* keys = A.alloc<u64>(n);
-  u64* skeys = A.alloc<u64>(n);
-  long long* idx = A.alloc<long long>(n);
-  long long* sidx = A.alloc<long long>(n);
-  int* first = A.alloc<int>(n);
-  u64* ukeys = A.alloc<u64>(n);
-  long long* upos = A.alloc<long long>(n);
-  long long* nsel = A.alloc<long long>(1);
-  long long* parent_pos = A.alloc<long long>(n);
-  // layer frames
-  int* lflag = A.alloc<int>(n);
-  long long* lay_index = A.alloc<long long>(n);
-  long long* lay = A.alloc<long long>(nl);
-  long long* d_np = A.alloc<long long>(nl);
-  int* cyclic = A.alloc<int>(1);
-  unsigned* pkey = A.alloc<unsigned>(nl);
-  unsigned* pkey2 = A.alloc<unsigned>(nl);
-  u64* skey = A.alloc<u64>(nl);
-  u64* skey2 = A.alloc<u64>(nl);
-  long long* ord = A.alloc<long long>(nl);
-  long long* ord2 = A.alloc<long long>(nl);
-  long long* off = A.alloc<long long>(nl + 2);
-  long long* jump[2] = {A.alloc<long long>(nl), A.alloc<long long>(nl)};
-  int* depth[2] = {A.alloc<int>(nl), A.alloc<int>(nl)};
-  int* sdepth = A.alloc<int>(nl);
-  long long* by_depth = A.alloc<long long>(nl);
-  long long* nodes = A.alloc<long long>(nl);
-  int* dmax = A.alloc<int>(1);
-  long long* size = A.alloc<long long>(nl);
-  long long* pre = A.alloc<long long>(nl);
-  long long* d_walk = A.alloc<long long>(nl);
-  long long* minus1 = A.alloc<long long>(1);
-  if (A.err != cudaSuccess) return perr(PM_ERR_CUDA, "pm_layer_tree: alloc");
-  size_t tmp = 0, t2 = 0;
-  cub::DeviceRadixSort::SortPairs(nullptr, tmp, keys, skeys, idx, sidx, (int64_t)n, 0, 64, s);
-  cub::DeviceSelect::Flagged(nullptr, t2, skeys, first, ukeys, nsel, (int64_t)n, s);
-  tmp = std::max(tmp, t2);
-  cub::DeviceScan::ExclusiveSum(nullptr, t2, lflag, lay_index, (int64_t)n, s);
-  tmp = std::max(tmp, t2);
-  cub::DeviceRadixSort::SortPairs(nullptr, t2, skey, skey2, ord, ord2, (int64_t)nl, 0, 64, s);
-  tmp = std::max(tmp, t2);
-  cub::DeviceRadixSort::SortPairs(nullptr, t2, depth[0], sdepth, ord, by_depth, (int64_t)nl, 0, 32, s);
-  tmp = std::max(tmp, t2);
-  cub::DeviceReduce::Max(nullptr, t2, depth[0], dmax, (int64_t)nl, s);
-  tmp = std::max(tmp, t2);
-  void* t = A.alloc<char>(tmp);
-  if (A.err != cudaSuccess) return perr(PM_ERR_CUDA, "pm_layer_tree: alloc");
-
-  pmp::k_pid_keys<<<blocks_for(n), 256, 0, s>>>(d_pid, n, keys, idx);
-  cub::DeviceRadixSort::SortPairs(t, tmp, keys, skeys, idx, sidx, (int64_t)n, 0, 64, s);
-  pmp::k_pid_first<<<blocks_for(n), 256, 0, s>>>(skeys, n, first);
-  cub::DeviceSelect::Flagged(t, tmp, skeys, first, ukeys, nsel, (int64_t)n, s);
-  cub::DeviceSelect::Flagged(t, tmp, sidx, first, upos, nsel, (int64_t)n, s);
-  long long nu = 0;
-  int rc = download(&nu, nsel, 1, s);
-  if (rc == PM_SUCCESS) rc = sync_check(s, "pm_layer_tree: ids");
-  if (rc != PM_SUCCESS) return rc;
-  pmp::k_pid_parent<<<blocks_for(n), 256, 0, s>>>(d_par, n, ukeys, upos, nu,
-                                                   parent_pos);
-  // layer positions and their index among layers (input is in event order)
-  pmp::k_u8_to_int<<<blocks_for(n), 256, 0, s>>>(d_isl, n, lflag);
-  cub::DeviceScan::ExclusiveSum(t, tmp, lflag, lay_index, (int64_t)n, s);
-  pmp::k_scatter_flagged<<<blocks_for(n), 256, 0, s>>>(lflag, lay_index, n, lay);
-  cudaMemsetAsync(cyclic, 0, sizeof(int), s);
-  pmp::k_layer_anc<<<blocks_for(nl), 256, 0, s>>>(lay, nl, d_pid, parent_pos,
-                                                   d_isl, lay_index, n, d_np,
-                                                   cyclic);
-  int h_cyc = 0;
-  rc = download(&h_cyc, cyclic, 1, s);
-  if (rc == PM_SUCCESS) rc = sync_check(s, "pm_layer_tree: ancestors");
-  if (rc != PM_SUCCESS) return rc;
-  if (h_cyc) return perr(PM_ERR_CYCLIC_PARENT, "parent chain revisits a python id");
-  // children in (start, event) order per parent: stable sort by start, then
-  // stable sort by parent slot (nodes are in event order to begin with)
-  pmp::k_gather_u64<<<blocks_for(nl), 256, 0, s>>>(d_start, lay, nl,
-                                                    0x8000000000000000ull, 0, skey);
-  pmp::k_iota<<<blocks_for(nl), 256, 0, s>>>(ord, nl);
-  if (event_id) {
-    // ties by event id rather than input order: sort by it first (LSD)
-    const long long* d_eid = (const long long*)A.upload(event_id, n);
-    u64* ekey = A.alloc<u64>(nl);
-    u64* ekey2 = A.alloc<u64>(nl);
-    long long* eord = A.alloc<long long>(nl);
-    if (A.err != cudaSuccess) return perr(PM_ERR_CUDA, "pm_layer_tree: alloc");
-    pmp::k_gather_u64<<<blocks_for(nl), 256, 0, s>>>(d_eid, lay, nl,
-                                                      0x8000000000000000ull, 0, ekey);
-    cub::DeviceRadixSort::SortPairs(t, tmp, ekey, ekey2, ord, eord, (int64_t)nl, 0, 64, s);
-    pmp::k_gather_u64<<<blocks_for(nl), 256, 0, s>>>(d_start, lay, nl, 0, 0, skey2);
-    // skey[i] = start of node eord[i] (biased)
-    pmp::k_gather_u64_idx<<<blocks_for(nl), 256, 0, s>>>(skey2, eord, nl,
-                                                          0x8000000000000000ull, skey);
-    cudaMemcpyAsync(ord, eord, nl * sizeof(long long), cudaMemcpyDeviceToDevice, s);
-  }
-  cub::DeviceRadixSort::SortPairs(t, tmp, skey, skey2, ord, ord2, (int64_t)nl, 0, 64, s);
-  pmp::k_gather_parent_key<<<blocks_for(nl), 256, 0, s>>>(d_np, ord2, nl, pkey);
-  cub::DeviceRadixSort::SortPairs(t, tmp, pkey, pkey2, ord2, ord, (int64_t)nl, 0, 32, s);
-  pmp::k_child_off<<<blocks_for(nl + 2), 256, 0, s>>>(pkey2, nl, off);
-  // depth (pointer jumping) and nodes grouped by depth
-  pmp::k_depth_init<<<blocks_for(nl), 256, 0, s>>>(d_np, nl, jump[0], depth[0]);
-  int cur = 0;
-  for (long long span = 1; span < 2 * nl; span *= 2) {
-    pmp::k_depth_step<<<blocks_for(nl), 256, 0, s>>>(jump[cur], depth[cur], nl,
-                                                     jump[cur ^ 1], depth[cur ^ 1]);
-    cur ^= 1;
-  }
-  pmp::k_depth_final<<<blocks_for(nl), 256, 0, s>>>(jump[cur], nl, depth[cur]);
-  pmp::k_iota<<<blocks_for(nl), 256, 0, s>>>(nodes, nl);
-  cub::DeviceRadixSort::SortPairs(t, tmp, depth[cur], sdepth, nodes, by_depth, (int64_t)nl, 0, 32, s);
-  cub::DeviceReduce::Max(t, tmp, depth[cur], dmax, (int64_t)nl, s);
-  int maxd = 0;
-  rc = download(&maxd, dmax, 1, s);
-  if (rc == PM_SUCCESS) rc = download(node_parent, (const int64_t*)d_np, nl, s);
-  if (rc == PM_SUCCESS) rc = download(child_order, (const int64_t*)ord, nl, s);
-  if (rc == PM_SUCCESS) rc = download(child_off, (const int64_t*)off, nl + 2, s);
-  if (rc == PM_SUCCESS) rc = sync_check(s, "pm_layer_tree: depth");
-  if (rc != PM_SUCCESS) return rc;
-  if (maxd < 0) return PM_SUCCESS;  // no frame reaches the root: empty walk
-  long long* lvl = A.alloc<long long>(maxd + 2);
-  if (A.err != cudaSuccess) return perr(PM_ERR_CUDA, "pm_layer_tree: alloc");
-  pmp::k_level_off<<<blocks_for(maxd + 2), 256, 0, s>>>(sdepth, nl, maxd, lvl);
-  std::vector<long long> h_lvl(maxd + 2);
-  rc = download(h_lvl.data(), lvl, maxd + 2, s);
-  if (rc == PM_SUCCESS) rc = sync_check(s, "pm_layer_tree: levels");
-  if (rc != PM_SUCCESS) return rc;
-  // subtree sizes bottom-up, pre-order positions top-down
-  for (int d = maxd; d >= 0; --d) {
-    const long long a = h_lvl[d], b = h_lvl[d + 1];
-    if (b > a)
-      pmp::k_subtree_level<<<blocks_for(32 * (b - a)), 256, 0, s>>>(by_depth + a, b - a,
-                                                              ord, off, size);
-  }
-  const long long m1 = -1;
-  cudaMemcpyAsync(minus1, &m1, sizeof(long long), cudaMemcpyHostToDevice, s);
-  pmp::k_preorder_level<<<1, 32, 0, s>>>(minus1, 1, ord, off, size, pre);
-  for (int d = 0; d < maxd; ++d) {
-    const long long a = h_lvl[d], b = h_lvl[d + 1];
-    if (b > a)
-      pmp::k_preorder_level<<<blocks_for(32 * (b - a)), 256, 0, s>>>(by_depth + a, b - a,
-                                                               ord, off, size, pre);
-  }
-  // reachable nodes: depth >= 0, i.e. by_depth[h_lvl[0] ..]
-  const long long r0 = h_lvl[0], nr = h_lvl[maxd + 1] - h_lvl[0];
-  pmp::k_scatter_walk<<<blocks_for(nr), 256, 0, s>>>(by_depth + r0, nr, pre, d_walk);
-  rc = download(walk, (const int64_t*)d_walk, nr, s);
-  if (rc != PM_SUCCESS) return rc;
-  if (n_walk) *n_walk = nr;
-  return sync_check(s, "pm_layer_tree");
-}
-
 }  // extern "C"
+
+// orchestration and layer-tree cores, their single-trace entry points
+// (pm_orchestrate, pm_layer_tree) and the batched pipeline (pm_pipeline_batch)
+#include "pipeline_batch.cuh"

@@ -34,7 +34,9 @@ class DeviceBatch:
         self.lib = _native.load_library()
         self.torch = torch
         self.device = torch.device("cuda", device)
-        reqs = np.ascontiguousarray(reqs, dtype=REQ_DTYPE)
+        on_device = isinstance(reqs, torch.Tensor)  # pm_req_t bytes already in HBM
+        if not on_device:
+            reqs = np.ascontiguousarray(reqs, dtype=REQ_DTYPE)
         offsets = np.ascontiguousarray(offsets, dtype=np.int64)
         cfgs = np.ascontiguousarray(cfgs, dtype=CFG_DTYPE)
         self.n_traces = len(offsets) - 1
@@ -47,7 +49,7 @@ class DeviceBatch:
             t = torch.from_numpy(np.ascontiguousarray(a).view(np.uint8))
             return t.to(self.device)
 
-        self.d_reqs = dev(reqs)
+        self.d_reqs = reqs if on_device else dev(reqs)
         self.d_offsets = dev(offsets)
         self.d_cfgs = dev(cfgs)
         self.d_cfg_of = dev(np.ascontiguousarray(cfg_of, dtype=np.int32)) \

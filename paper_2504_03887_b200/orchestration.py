@@ -213,19 +213,23 @@ def _block_id(tag: int, a: int, b: int):
     return f"clone{a}:{b}"
 
 
-def build_sequence(analyzed: AnalyzedTrace, iterations: int = 2,
-                   ) -> RequestSequence:
-    """Assemble the replayable request sequence (orchestration.py:237-399)."""
+class _Plan:
+    """The host half of build_sequence for one trace: iteration windows,
+    optimizer spans, cloned markers, zero-grad marks and the batch requests
+    (a handful of markers; orchestration.py:237-336)."""
+
+
+def plan_sequence(markers, sidecar, iterations: int) -> _Plan:
+    """Raises what build_sequence raises before touching the blocks."""
     if iterations < 1:
         raise NoIterations(f"iterations must be >= 1, got {iterations}")
-    sidecar = analyzed.bundle.metadata
     if sidecar is None:
         raise MissingBatchBytes(
             "orchestration requires a sidecar (param_sizes, batch_bytes)")
-    steps = analyzed.steps()
+    steps = sorted((m for m in markers if m.kind is MarkerKind.PROFILER_STEP),
+                   key=lambda m: m.iteration_index)
     if not steps:
         raise NoIterations("trace has no iteration markers")
-    lk = analyzed._link
     n_trace = len(steps)
     include = min(iterations, n_trace)
     clones = iterations - include
@@ -235,12 +239,12 @@ def build_sequence(analyzed: AnalyzedTrace, iterations: int = 2,
         end = steps[k + 1].start_ts if k + 1 < n_trace else steps[k].end_ts
         windows.append((start, end))
 
-    spans = [m for m in analyzed.markers if m.kind is MarkerKind.OPTIMIZER_STEP]
+    spans = [m for m in markers if m.kind is MarkerKind.OPTIMIZER_STEP]
     tpl = windows[-1]
     width = tpl[1] - tpl[0]
     clone_markers = []
     if clones:
-        tpl_markers = [m for m in analyzed.markers
+        tpl_markers = [m for m in markers
                        if m.iteration_index == include - 1
                        and tpl[0] <= m.start_ts < tpl[1]]
         for c in range(1, clones + 1):
@@ -248,7 +252,7 @@ def build_sequence(analyzed: AnalyzedTrace, iterations: int = 2,
                 clone_markers.append(AnnotationMarker(
                     m.kind, m.start_ts + width * c, m.end_ts + width * c,
                     include - 1 + c))
-    all_markers = list(analyzed.markers) + clone_markers
+    all_markers = list(markers) + clone_markers
     zg = sorted(m.start_ts for m in all_markers if m.kind is MarkerKind.ZERO_GRAD)
     step_markers = sorted((m for m in all_markers
                            if m.kind is MarkerKind.PROFILER_STEP
@@ -262,20 +266,43 @@ def build_sequence(analyzed: AnalyzedTrace, iterations: int = 2,
             bk += [0, 1]
             bi += [step.iteration_index] * 2
             bj += [j, j]
+    p = _Plan()
+    p.spans = ([m.start_ts for m in spans], [m.end_ts for m in spans],
+               [m.iteration_index for m in spans])
+    p.param_sizes = sorted(set(sidecar.param_sizes))
+    p.windows = ([w[0] for w in windows], [w[1] for w in windows])
+    p.zg = zg
+    p.clones = clones
+    p.tpl = tpl if clones else (0, 0)
+    p.shift = width
+    p.batch = (bv, bs, bk, bi, bj)
+    p.batch_ids = list(zip(bi[::2], bj[::2]))
+    p.has_batch_bytes = bool(sidecar.batch_bytes)
+    boundaries = [w[0] for w in windows]
+    end = windows[-1][1]
+    if clones:
+        for c in range(1, clones + 1):
+            boundaries.append(windows[-1][0] + width * c)
+        end = windows[-1][0] + width * (clones + 1)
+    boundaries.append(end)
+    p.boundaries = boundaries
+    return p
 
+
+def build_sequence(analyzed: AnalyzedTrace, iterations: int = 2,
+                   ) -> RequestSequence:
+    """Assemble the replayable request sequence (orchestration.py:237-399)."""
+    plan = plan_sequence(analyzed.markers, analyzed.bundle.metadata, iterations)
+    lk = analyzed._link
     nb = int(lk.n_blocks)
     role_codes = lk.b_role if nb else np.zeros(0, np.int32)
     o = _pipeline.orchestrate(
-        lk.b_alloc, lk.b_size, lk.b_free, role_codes,
-        ([m.start_ts for m in spans], [m.end_ts for m in spans],
-         [m.iteration_index for m in spans]),
-        sorted(set(sidecar.param_sizes)),
-        ([w[0] for w in windows], [w[1] for w in windows]), zg, clones,
-        tpl if clones else (0, 0), width,
-        (bv, bs, bk, bi, bj))
+        lk.b_alloc, lk.b_size, lk.b_free, role_codes, plan.spans,
+        plan.param_sizes, plan.windows, plan.zg, plan.clones, plan.tpl,
+        plan.shift, plan.batch)
     if o.n < 0:
         raise NoGradientBlocks("no backward-retained blocks in trace")
-    if not sidecar.batch_bytes:
+    if not plan.has_batch_bytes:
         raise MissingBatchBytes("sidecar provides no batch tensor sizes")
 
     # the reference mutates the analyzed blocks in place
@@ -284,17 +311,10 @@ def build_sequence(analyzed: AnalyzedTrace, iterations: int = 2,
         analyzed._apply_final()
     arrays = {"n": o.n, "n_model": o.n_model, "kind": o.kind, "size": o.size,
               "vts": o.vts, "tag": o.tag, "a": o.a, "b": o.b, "role": o.role,
-              "raw": o.raw, "batch_ids": list(zip(bi[::2], bj[::2]))}
-    boundaries = [w[0] for w in windows]
-    end = windows[-1][1]
-    if clones:
-        for c in range(1, clones + 1):
-            boundaries.append(windows[-1][0] + width * c)
-        end = windows[-1][0] + width * (clones + 1)
-    boundaries.append(end)
-    return RequestSequence(iteration_boundaries=boundaries, packed=o.packed,
+              "raw": o.raw, "batch_ids": plan.batch_ids}
+    return RequestSequence(iteration_boundaries=plan.boundaries, packed=o.packed,
                            arrays=arrays)
 
 
 __all__ = ["AnalyzedTrace", "MemoryRequest", "RequestKind", "RequestSequence",
-           "analyze", "build_sequence", "LayerMemoryProfile"]
+           "analyze", "build_sequence", "plan_sequence", "LayerMemoryProfile"]
