@@ -270,8 +270,8 @@ class LayerTreeColumns:
         names = bundle.names
         table = getattr(names, "table", None)
         if table is not None:  # name-id view: test each distinct name once
-            flag = np.array([_is_layer(t, LAYER_NAME_PREFIXES) for t in table])
-            is_layer = flag[names.ids[idx]]
+            flag = names.table_flags(LAYER_NAME_PREFIXES)
+            is_layer = flag[names.ids[idx]] if len(flag) else np.zeros(len(idx), bool)
         else:
             is_layer = np.fromiter((_is_layer(names[i], LAYER_NAME_PREFIXES)
                                     for i in idx.tolist()), bool, len(idx))

@@ -33,9 +33,6 @@ from .errors import (CyclicParentLink, MissingBatchBytes, NoGradientBlocks,
 from .orchestration import plan_sequence
 from .trace import NONE, EventCategory, TraceBundle
 
-# the column order of the single host -> device upload
-_COLS = ("fn_pid", "fn_par", "fn_start", "fn_end", "op_start", "op_end",
-         "op_seq", "in_start", "in_addr", "in_nbytes")
 
 
 @dataclass
@@ -47,30 +44,37 @@ class _Trace:
 
 
 def _is_layer_column(bundle: TraceBundle, idx: np.ndarray) -> np.ndarray:
+    """The layer-name test (analysis.py:115-182) once per distinct name."""
     names = bundle.names
-    table = getattr(names, "table", None)
-    if table is not None:  # name-id view: test each distinct name once
-        flag = np.array([_is_layer(t, LAYER_NAME_PREFIXES) for t in table], bool)
+    if hasattr(names, "table_flags"):
+        flag = names.table_flags(LAYER_NAME_PREFIXES)
         return flag[names.ids[idx]] if len(flag) else np.zeros(len(idx), bool)
     return np.fromiter((_is_layer(names[i], LAYER_NAME_PREFIXES)
                         for i in idx.tolist()), bool, len(idx))
 
 
+# (column, category, bundle field) of the single host -> device upload;
+# gathered straight into the pinned staging buffer
+_GATHER = (("fn_pid", "fn", "python_id"), ("fn_par", "fn", "parent_id"),
+           ("fn_start", "fn", "start"), ("fn_end", "fn", "end"),
+           ("op_start", "op", "start"), ("op_end", "op", "end"),
+           ("op_seq", "op", "sequence_number"), ("in_start", "in", "start"),
+           ("in_addr", "in", "addr"), ("in_nbytes", "in", "nbytes"))
+_CAT = {"fn": EventCategory.PYTHON_FUNCTION, "op": EventCategory.CPU_OP,
+        "in": EventCategory.CPU_INSTANT_EVENT}
+
+
+def _column(bundle: TraceBundle, field: str) -> np.ndarray:
+    if field == "start":
+        return bundle.start
+    if field == "end":
+        return bundle.end
+    return bundle.ints[field]
+
+
 def _trace(bundle: TraceBundle, iterations: int) -> _Trace:
-    fn = bundle.indices(EventCategory.PYTHON_FUNCTION)
-    ops = bundle.indices(EventCategory.CPU_OP)
-    inst = bundle.indices(EventCategory.CPU_INSTANT_EVENT)
-    seq = bundle.ints["sequence_number"][ops]
-    cols = {
-        "fn_pid": bundle.ints["python_id"][fn], "fn_par": bundle.ints["parent_id"][fn],
-        "fn_start": bundle.start[fn], "fn_end": bundle.end[fn],
-        "fn_is_layer": _is_layer_column(bundle, fn),
-        "op_start": bundle.start[ops], "op_end": bundle.end[ops],
-        "op_seq": np.where(seq == NONE, -1, seq),
-        "in_start": bundle.start[inst], "in_addr": bundle.ints["addr"][inst],
-        "in_nbytes": bundle.ints["nbytes"][inst],
-    }
-    tr = _Trace(cols)
+    idx = {k: bundle.indices(c) for k, c in _CAT.items()}
+    tr = _Trace({"idx": idx, "bundle": bundle})
     try:
         markers = extract_markers(bundle.by_category(EventCategory.USER_ANNOTATION))
     except NoIterationMarkers as e:
@@ -127,33 +131,42 @@ def build_sequences(bundles, iterations: int = 2, device: int = 0) -> SequenceBa
     if B == 0:
         raise ValueError("build_sequences needs at least one trace")
     traces = [_trace(b, iterations) for b in bundles]
-    nf = np.array([len(t.cols["fn_pid"]) for t in traces], np.int64)
-    no = np.array([len(t.cols["op_start"]) for t in traces], np.int64)
-    ni = np.array([len(t.cols["in_start"]) for t in traces], np.int64)
+    counts = {k: np.array([len(t.cols["idx"][k]) for t in traces], np.int64)
+              for k in _CAT}
 
     def offs(counts):
         o = np.zeros(len(counts) + 1, np.int64)
         np.cumsum(counts, out=o[1:])
         return o
 
-    fn_off, op_off, in_off = offs(nf), offs(no), offs(ni)
-    sizes = {"fn": int(fn_off[-1]), "op": int(op_off[-1]), "in": int(in_off[-1])}
-    # one pinned host buffer -> one upload
-    lens = [sizes[c.split("_")[0]] for c in _COLS]
-    total = sum(lens) + (sizes["fn"] + 7) // 8
+    fn_off, op_off, in_off = offs(counts["fn"]), offs(counts["op"]), offs(counts["in"])
+    tot = {"fn": int(fn_off[-1]), "op": int(op_off[-1]), "in": int(in_off[-1])}
+    toff = {"fn": fn_off, "op": op_off, "in": in_off}
+    # one pinned host buffer (columns gathered straight into it) -> one upload
+    total = sum(tot[k] for _, k, _ in _GATHER) + (tot["fn"] + 7) // 8
     dev = torch.device("cuda", device)
     h = torch.empty(max(total, 1), dtype=torch.int64, pin_memory=True)
     hv = h.numpy()
     pos = {}
     at = 0
-    for c, n in zip(_COLS, lens):
-        if n:
-            np.concatenate([t.cols[c] for t in traces], out=hv[at:at + n])
-        pos[c] = (at, n)
-        at += n
+    for col, k, field in _GATHER:
+        for t, tr in enumerate(traces):
+            a, z = at + int(toff[k][t]), at + int(toff[k][t + 1])
+            if z > a:
+                np.take(_column(tr.cols["bundle"], field), tr.cols["idx"][k],
+                        out=hv[a:z])
+        pos[col] = (at, tot[k])
+        at += tot[k]
+    # sequence numbers: None -> -1 (the kernels' "no sequence number")
+    a, n = pos["op_seq"]
+    if n:
+        seqv = hv[a:a + n]
+        seqv[seqv == NONE] = -1
     isl = hv[at:].view(np.uint8)
-    if sizes["fn"]:
-        isl[:sizes["fn"]] = np.concatenate([t.cols["fn_is_layer"] for t in traces])
+    for t, tr in enumerate(traces):
+        a, z = int(fn_off[t]), int(fn_off[t + 1])
+        if z > a:
+            isl[a:z] = _is_layer_column(tr.cols["bundle"], tr.cols["idx"]["fn"])
     d = h.to(dev, non_blocking=True)
     base = d.data_ptr()
 
@@ -167,9 +180,9 @@ def build_sequences(bundles, iterations: int = 2, device: int = 0) -> SequenceBa
         return a.ctypes.data if a.size else None
 
     desc.fn_off, desc.op_off, desc.in_off = host(fn_off), host(op_off), host(in_off)
-    for c in _COLS:
+    for c, _, _ in _GATHER:
         setattr(desc, c, base + 8 * pos[c][0] if pos[c][1] else None)
-    desc.fn_is_layer = base + 8 * at if sizes["fn"] else None
+    desc.fn_is_layer = base + 8 * at if tot["fn"] else None
 
     # per-trace orchestration parameters (CSR)
     empty = ([], [], [])
@@ -202,7 +215,7 @@ def build_sequences(bundles, iterations: int = 2, device: int = 0) -> SequenceBa
 
     # requests per trace <= model (<= blocks) + batch + 2 blocks (1 + clones)
     bat_counts = np.array([len(b[0]) for b in bt], np.int64)
-    cap = int((ni * (3 + 2 * clones.astype(np.int64)) + bat_counts).sum()) + 16
+    cap = int((counts["in"] * (3 + 2 * clones.astype(np.int64)) + bat_counts).sum()) + 16
     rs = _native.REQ_DTYPE.itemsize
     d_reqs = torch.empty(cap * rs, dtype=torch.uint8, device=dev)
     req_off, status, n_model, bd = _pipeline.pipeline_batch(

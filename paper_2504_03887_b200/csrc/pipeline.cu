@@ -421,30 +421,69 @@ __global__ void k_leaf_keys(const long long* lstart, long long n, u64* keys,
 
 // For each root: among leaves with lstart <= rstart and rend <= lend, the
 // smallest duration, ties -> first in walk order (linking.py:56-64).
-// Leaves sorted by start; a backward scan stops once the prefix max of leaf
-// ends drops below rend.
+// One warp per root, warp-cooperative: the leaves are sorted by start with
+// an inclusive prefix max of their ends; the lanes binary-search the last
+// leaf starting at or before the root 32-ary (one probe per lane per round),
+// then scan backwards 32 leaves per step.  The prefix max only falls going
+// backwards, so the scan ends at the first step where some lane's prefix
+// max is below the root's end (no earlier leaf can contain it).
 __global__ void k_link_fwd(const long long* sl_start, const long long* sl_w,
                            const long long* sl_pmax_end,
                            const long long* lstart, const long long* lend,
                            long long nl, const long long* rstart,
                            const long long* rend, long long nr,
                            long long* root_leaf) {
-  long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (r >= nr) return;
+  const long long r = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (r >= nr) return;  // whole warp
   const long long s = rstart[r], e = rend[r];
-  long long i = upper_bound_ll(sl_start, nl, s) - 1;
+  // upper_bound(sl_start, s) by 32-ary search: [lo, hi) holds the answer
+  long long lo = 0, hi = nl;
+  while (hi - lo > 32) {
+    const long long step = (hi - lo + 31) / 32;
+    const long long k = lo + lane * step;
+    const unsigned b = __ballot_sync(0xffffffffu, k < hi && sl_start[k] <= s);
+    if (b == 0) {
+      hi = lo;  // sl_start[lo] > s
+      break;
+    }
+    const int last = 31 - __clz(b);
+    lo += last * step;
+    hi = min(lo + step, hi);
+    lo += 1;  // sl_start[lo - 1] <= s
+  }
+  if (hi > lo) {
+    const long long k = lo + lane;
+    const unsigned b = __ballot_sync(0xffffffffu, k < hi && sl_start[k] <= s);
+    lo += b ? 32 - __clz(b) : 0;
+  }
+  // lo = upper_bound: leaves [0, lo) start at or before the root
   long long best = -1, bdur = 0;
-  for (; i >= 0 && sl_pmax_end[i] >= e; --i) {
-    const long long w = sl_w[i];
-    if (lend[w] >= e) {
-      const long long dur = lend[w] - lstart[w];
-      if (best < 0 || dur < bdur || (dur == bdur && w < best)) {
-        best = w;
-        bdur = dur;
+  for (long long base = lo - 1; base >= 0; base -= 32) {
+    const long long i = base - lane;
+    const bool ok = i >= 0 && sl_pmax_end[i] >= e;
+    if (ok) {
+      const long long w = sl_w[i];
+      if (lend[w] >= e) {
+        const long long dur = lend[w] - lstart[w];
+        if (best < 0 || dur < bdur || (dur == bdur && w < best)) {
+          best = w;
+          bdur = dur;
+        }
       }
     }
+    if (!__all_sync(0xffffffffu, ok)) break;
   }
-  root_leaf[r] = best;
+  // warp argmin of (duration, walk index) over the lanes' candidates
+  for (int o = 16; o > 0; o >>= 1) {
+    const long long ob = __shfl_down_sync(0xffffffffu, best, o);
+    const long long od = __shfl_down_sync(0xffffffffu, bdur, o);
+    if (ob >= 0 && (best < 0 || od < bdur || (od == bdur && ob < best))) {
+      best = ob;
+      bdur = od;
+    }
+  }
+  if (lane == 0) root_leaf[r] = best;
 }
 
 // ---- a9: backward ops by sequence number ------------------------------------
@@ -1213,8 +1252,8 @@ int stage_join(Arena& A, const RootsDev& R, long long nl,
   }
   if (nr > 0) {
     if (nl > 0)
-      k_link_fwd<<<blocks_for(nr, 128), 128, 0, s>>>(sl_start, lidx, sl_pmax, d_lstart, d_lend, nl,
-                                                     R.start, R.end, nr, J->root_leaf);
+      k_link_fwd<<<blocks_for(32 * nr), 256, 0, s>>>(sl_start, lidx, sl_pmax, d_lstart, d_lend,
+                                                     nl, R.start, R.end, nr, J->root_leaf);
     else
       cudaMemsetAsync(J->root_leaf, 0xff, sizeof(long long) * nr, s);
   }

@@ -208,7 +208,11 @@ struct NDir {
       }
       if (p >= cta_buckets) p = -1;
     }
-    return __shfl_sync(kFull, p, 0);
+    p = __shfl_sync(kFull, p, 0);
+    // lane 0's acquire (atomic + fence) reaches the other lanes through the
+    // warp barrier's memory ordering before any of them touches the bucket
+    __syncwarp();
+    return p;
   }
   // The CTA's pool is exhausted: wait for another warp to hand a bucket
   // back (buckets empty out continuously as free blocks are taken).  If

@@ -33,7 +33,7 @@ def test_analysis_error_wins_over_digest_error(monkeypatch):
         metadata = None
 
     with pytest.raises(Analysis):
-        PeakMemoryEstimator().estimate(Bundle())
+        PeakMemoryEstimator().estimate_with_details(Bundle(), _timeline=False)
 
 
 def test_digest_error_surfaces_after_the_pipeline(monkeypatch):
@@ -62,6 +62,85 @@ def test_digest_error_surfaces_after_the_pipeline(monkeypatch):
         metadata = None
 
     with pytest.raises(ValueError, match="digest"):
-        PeakMemoryEstimator().estimate(Bundle())
-    # the whole device pipeline ran first; estimate() asks for no timeline
+        PeakMemoryEstimator().estimate_with_details(Bundle(), _timeline=False)
+    # the whole device pipeline ran first; no timeline was asked for
     assert calls == ["analyze", "build", ("replay", False)]
+
+
+class _FakeSeqs:
+    """batch.SequenceBatch stand-in: per-trace errors, empty sequences."""
+
+    def __init__(self, errors):
+        import numpy as np
+        self.errors = errors
+        self.req_off = np.zeros(len(errors) + 1, np.int64)
+        self.d_reqs = None
+
+    def breakdown(self, t):
+        return {}
+
+    def packed(self, t):
+        return None
+
+
+def _fake_device_batch(calls):
+    import numpy as np
+    from paper_2504_03887_b200._native import RESULT_DTYPE
+
+    class DB:
+        def __init__(self, reqs, offs, cfgs, cfg_of):
+            self.n = len(offs) - 1
+
+        def launch(self):
+            calls.append("replay")
+
+        def results(self):
+            return np.zeros(self.n, RESULT_DTYPE)
+
+    return DB
+
+
+def test_estimate_many_pipeline_error_wins_over_digest_error(monkeypatch):
+    from paper_2504_03887_b200 import batch, engine
+
+    class Analysis(Exception):
+        pass
+
+    calls = []
+    monkeypatch.setattr(batch, "build_sequences",
+                        lambda b, iterations: _FakeSeqs([None, Analysis("a")]))
+    monkeypatch.setattr(engine, "DeviceBatch", _fake_device_batch(calls))
+    monkeypatch.setattr(PeakMemoryEstimator, "_digest",
+                        lambda self, *a: (_ for _ in ()).throw(ValueError("digest")))
+
+    class Bundle:
+        metadata = None
+
+    # trace 0 succeeds up to its digest, which raises first (bundle order)
+    with pytest.raises(ValueError, match="digest"):
+        PeakMemoryEstimator().estimate_many([Bundle(), Bundle()])
+    got = PeakMemoryEstimator().estimate_many([Bundle(), Bundle()],
+                                              return_exceptions=True)
+    assert isinstance(got[0], ValueError) and isinstance(got[1], Analysis)
+    # a failing pipeline alone: its error, never the digest's
+    monkeypatch.setattr(batch, "build_sequences",
+                        lambda b, iterations: _FakeSeqs([Analysis("a")]))
+    with pytest.raises(Analysis):
+        PeakMemoryEstimator().estimate_many([Bundle()])
+
+
+def test_estimate_many_digest_error_after_replay(monkeypatch):
+    from paper_2504_03887_b200 import batch, engine
+    calls = []
+    monkeypatch.setattr(batch, "build_sequences",
+                        lambda b, iterations: calls.append("build") or _FakeSeqs([None]))
+    monkeypatch.setattr(engine, "DeviceBatch", _fake_device_batch(calls))
+    monkeypatch.setattr(PeakMemoryEstimator, "_digest",
+                        lambda self, *a: (_ for _ in ()).throw(ValueError("digest")))
+
+    class Bundle:
+        metadata = None
+
+    with pytest.raises(ValueError, match="digest"):
+        PeakMemoryEstimator().estimate(Bundle())
+    assert calls == ["build", "replay"]

@@ -23,6 +23,10 @@ def main():
     ap.add_argument("--leaves", type=int, nargs="+", default=[6000])
     ap.add_argument("--iterations", type=int, default=2)
     ap.add_argument("--check", action="store_true")
+    ap.add_argument("--sweep", type=int, default=0,
+                    help="also: N event-level traces (leaves 200 k, k = 1..N) "
+                         "estimated in one estimate_many call vs a loop of "
+                         "per-trace estimate_with_details")
     ap.add_argument("--file", action="store_true",
                     help="also time the user path: write the trace as chrome "
                          "JSON, then parse_trace + estimate from the file")
@@ -38,6 +42,22 @@ def main():
     b0 = synth_events.generate(50, args.iterations)
     replay_sequence(api.build_sequence(api.analyze(b0), args.iterations),
                     api.AllocatorConfig())
+    if args.sweep:
+        bs = [synth_events.generate(200 * k, args.iterations, seed=k)
+              for k in range(1, args.sweep + 1)]
+        est = api.PeakMemoryEstimator(iterations=args.iterations)
+        est.estimate_many(bs[:2])
+        t0 = time.perf_counter()
+        many = est.estimate_many(bs)
+        t1 = time.perf_counter()
+        loop = [est.estimate_with_details(b, _timeline=False)[0] for b in bs]
+        t2 = time.perf_counter()
+        print(json.dumps({
+            "sweep_traces": len(bs), "events": sum(len(b) for b in bs),
+            "requests": sum(r.sequence_length for r in many),
+            "estimate_many_s": t1 - t0, "per_trace_loop_s": t2 - t1,
+            "reports_equal": all(a.canonical_json() == b.canonical_json()
+                                 for a, b in zip(many, loop))}), flush=True)
     for leaves in args.leaves:
         t0 = time.perf_counter()
         b = synth_events.generate(leaves, args.iterations)
@@ -49,7 +69,22 @@ def main():
         res = replay_sequence(seq, api.AllocatorConfig(), timeline=False)
         t4 = time.perf_counter()
         n = len(b)
-        line = {"leaves": leaves, "events": n, "requests": len(seq.requests),
+        # the batched, device-resident path (pm_pipeline_batch) on the same
+        # trace: analyze + build_sequence in one call
+        from paper_2504_03887_b200.batch import build_sequences
+        build_sequences([b], args.iterations)  # warm (pool growth at this size)
+        t5 = time.perf_counter()
+        sb = build_sequences([b], args.iterations)
+        torch.cuda.synchronize()
+        t6 = time.perf_counter()
+        batch_equal = bool((sb.packed(0) == seq.packed).all())
+        t7 = time.perf_counter()
+        rep_b = api.PeakMemoryEstimator(iterations=args.iterations).estimate_many([b])[0]
+        t8 = time.perf_counter()
+        line = {"leaves": leaves, "events": n, "requests": len(seq.packed),
+                "batch_analyze_build_s": t6 - t5, "batch_equal": batch_equal,
+                "estimate_many_s": t8 - t7,
+                "estimate_many_peak_equal": rep_b.reserved_peak == res.peak_reserved,
                 "gen_s": t1 - t0, "analyze_s": t2 - t1,
                 "build_sequence_s": t3 - t2, "replay_s": t4 - t3,
                 "pipeline_events_per_s": n / (t4 - t1),
