@@ -149,14 +149,23 @@ def build_sequences(bundles, iterations: int = 2, device: int = 0) -> SequenceBa
     hv = h.numpy()
     pos = {}
     at = 0
+    jobs = []
     for col, k, field in _GATHER:
         for t, tr in enumerate(traces):
             a, z = at + int(toff[k][t]), at + int(toff[k][t + 1])
             if z > a:
-                np.take(_column(tr.cols["bundle"], field), tr.cols["idx"][k],
-                        out=hv[a:z])
+                jobs.append((_column(tr.cols["bundle"], field), tr.cols["idx"][k],
+                             hv[a:z]))
         pos[col] = (at, tot[k])
         at += tot[k]
+    # numpy's take releases the GIL: the column gathers run on host threads
+    if len(jobs) > 1 and sum(len(j[1]) for j in jobs) > (1 << 20):
+        from concurrent.futures import ThreadPoolExecutor
+        with ThreadPoolExecutor(max_workers=min(len(jobs), 16)) as pool:
+            list(pool.map(lambda j: np.take(j[0], j[1], out=j[2]), jobs))
+    else:
+        for src, idx, out in jobs:
+            np.take(src, idx, out=out)
     # sequence numbers: None -> -1 (the kernels' "no sequence number")
     a, n = pos["op_seq"]
     if n:
