@@ -1,0 +1,7 @@
+# iteration: build, replay + pipeline parity, C3 timing (10^4 traces), C4, fragmented
+set -x
+python -c "import __graft_entry__ as g; g.build()" 2>&1 | tail -2
+timeout 900 python -m pytest -x -q -m gpu tests/test_replay_gpu.py tests/test_replay_narrow_gpu.py tests/test_config_goldens.py tests/test_c4_sweep.py tests/test_handoff_gpu.py tests/test_validate_gpu.py ${EXTRA_TESTS} 2>&1 | tail -3
+for i in 1 2; do timeout 300 python tools/prof_replay.py --traces 10000 --launches 3 2>&1 | tail -1; done
+timeout 600 python tools/bench_c4.py 2>&1 | tail -1
+timeout 600 python tools/bench_frag.py 2>&1 | tail -1
