@@ -1108,28 +1108,10 @@ __device__ __forceinline__ void replay_trace(
                 sg.bar + buf);
     }
   };
-  if (lane == 0 && r0 < n && k0 < nchunks) fetch(k0, sg.g & 1);
+  if (lane == 0 && k0 < nchunks) fetch(k0, sg.g & 1);
 
-  // One loop over the requests; the chunk prologue runs at each chunk
-  // boundary (a uniform branch).  A single loop level keeps every early exit
-  // (error status, hand-off) a one-level break.
-  int cbase = 0;
-  int k = k0 - 1;  // current chunk
-  ulonglong2* cb = sg.buf;
-  int hcmp = -1;
-  bool fresh = false;
-  uint4* myrec = rec.rec(0u);
-  uint4* const st = sg.rec;
-  uint4 ev_next = make_uint4(0, 0, 0, 0);
-  for (int rq = r0; rq < n; ++rq) {
-   const int j = rq & 31;
-   if (j == 0 || k < k0) {
-    if (k >= k0) {  // the previous chunk is consumed
-      __syncwarp();
-      sg.g += 1;
-    }
-    k = rq >> 5;
-    cbase = 32 * k;
+  for (int k = k0; k < nchunks; ++k) {
+    const int cbase = 32 * k;
     if (wire) {
       __syncwarp();
       ws->abase_chunk = abase;  // uniform store: a checkpoint's resume point
@@ -1140,7 +1122,7 @@ __device__ __forceinline__ void replay_trace(
       // prefetch the next chunk into the other buffer (consumed last chunk)
       fetch(k + 1, b ^ 1);
     }
-    cb = sg.buf + 32 * b;
+    ulonglong2* cb = sg.buf + 32 * b;
     const int cnt = min(n - cbase, 32);
     if (wire) {
       // decode the chunk's wire words in place into pm_req_t form
@@ -1179,7 +1161,7 @@ __device__ __forceinline__ void replay_trace(
     const ulonglong2 evl = lane < cnt ? cb[lane] : make_ulonglong2(0ull, 0ull);
     const int my_h = lane < cnt ? (int)lo(evl.y) : -1;
     const bool hok = my_h >= 0 && my_h < n;
-    fresh = hok && my_h > wm;
+    const bool fresh = hok && my_h > wm;
     {
       const int cmax = __reduce_max_sync(kFull, hok ? my_h : -1);
       if (cmax > wm) {
@@ -1197,15 +1179,16 @@ __device__ __forceinline__ void replay_trace(
       }
     }
     uint4 r = make_uint4(0, 0, 0, 0);
-    myrec = rec.rec((u32)(hok ? my_h : 0));
+    uint4* const myrec = rec.rec((u32)(hok ? my_h : 0));
     if (hok && !fresh) r = *myrec;
 #ifdef PM_VALIDATE
     // the validator reads every record <= wm: a fresh handle's record is
     // "never allocated" from the start of its chunk
     if (fresh) *myrec = r;
 #endif
+    uint4* st = sg.rec;
     st[lane] = r;
-    hcmp = hok ? my_h : -1;
+    const int hcmp = hok ? my_h : -1;
     {
       const unsigned kind_l = hi(evl.y) & 3u;
       int pre = PM_OK;
@@ -1238,9 +1221,10 @@ __device__ __forceinline__ void replay_trace(
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
     __syncwarp();
-    ev_next = reinterpret_cast<const uint4*>(cb)[j];
-   }
-    {
+
+    const int j0 = k == k0 ? (r0 & 31) : 0;
+    uint4 ev_next = reinterpret_cast<const uint4*>(cb)[j0];
+    for (int j = j0; j < cnt; ++j) {
       // the next request's word is loaded before this one's dependent chain
       // (slot 32 lies inside the staging area: read, never used)
       const uint4 ev = ev_next;
@@ -1463,17 +1447,18 @@ __device__ __forceinline__ void replay_trace(
           if (fresh && (done_l >> lane & 1u) == 0u && (same & done_l) == 0u)
             *myrec = make_uint4(0, 0, 0, 0);
         }
-        break;  // the checkpoint is written after the request loop
+        break;  // the checkpoint is written after the chunk loop
       }
     }
-  }
-  if (k >= k0) {  // the last chunk started is consumed
     __syncwarp();
     sg.g += 1;
-    if (status != PM_OK && k + 1 < nchunks) {
-      // drain the prefetch in flight so the buffer's phase stays in step
-      mbar_wait(sg.bar + (sg.g & 1), (sg.g >> 1) & 1);
-      sg.g += 1;
+    if (status != PM_OK) {
+      if (k + 1 < nchunks) {
+        // drain the prefetch in flight so the buffer's phase stays in step
+        mbar_wait(sg.bar + (sg.g & 1), (sg.g >> 1) & 1);
+        sg.g += 1;
+      }
+      break;
     }
   }
 
