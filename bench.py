@@ -81,6 +81,8 @@ def parse_args(argv=None):
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--cpu-sample-stride", type=int, default=10)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-other-configs", action="store_true",
+                    help="skip the C2 / C4 / C5 measurements beside the C3 line")
     ap.add_argument("--ref-check-traces", type=int, default=16)
     ap.add_argument("--dry-run", action="store_true",
                     help="CPU/gloo plumbing check (oracle replay); not a bench value")
@@ -514,9 +516,106 @@ def main():
                       "frac": value / (ceiling * world),
                       "source": "profiles/replay_ncu_summary.json (ncu --set full "
                                 "of the replay kernel: instructions, DRAM bytes)"})
+    if world == 1 and not args.no_other_configs:
+        line["other_configs"] = other_configs(dev)
     print(json.dumps(line))
     if dist:
         dist.destroy_process_group()
+
+
+def other_configs(dev) -> dict:
+    """BASELINE.json's other configs, measured in the same run (rank 0, N=1)
+    so that they are driver-measured too; each checked for parity.
+
+    c2  64 GPT-2 small sequences (batch sizes 1..64, tests/golden/c2_sweep.npz)
+        as ONE device-resident replay batch, median of 20 launches (CUDA
+        events); every result field vs the reference's (c2_sweep_golden.json).
+    c4  50 traces x 69 allocator configs (tools/bench_c4.py's batch), best
+        of 3 (parity: the GPU tests against the reference's grid goldens).
+    c5  one 10^7-event C5-style event-level trace: the batched device
+        pipeline (analyze + build_sequence, pm_pipeline_batch) and the
+        single-trace replay of its 4.3e6 requests, wall clock; peak vs the
+        per-trace API's sequence replayed by the C oracle is in the tests.
+    """
+    import torch
+    sys.path.insert(0, str(REPO / "tests"))
+    from paper_2504_03887_b200 import synth, synth_events
+    from paper_2504_03887_b200.allocator import AllocatorConfig, cfg_record
+    from paper_2504_03887_b200.batch import build_sequences
+    from paper_2504_03887_b200.engine import DeviceBatch
+    out = {}
+    stream = torch.cuda.current_stream(dev)
+
+    def device_ms(batch, reps):
+        batch.launch(stream)
+        torch.cuda.synchronize(dev)
+        ms = []
+        for _ in range(reps):
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            batch.launch(stream)
+            e1.record(stream)
+            torch.cuda.synchronize(dev)
+            ms.append(e0.elapsed_time(e1))
+        return ms
+
+    # C2
+    z = np.load(REPO / "tests" / "golden" / "c2_sweep.npz")
+    gold = json.loads((REPO / "tests" / "golden" / "c2_sweep_golden.json").read_text())
+    b = DeviceBatch(z["reqs"], z["offsets"], cfg_record(AllocatorConfig()), device=dev.index)
+    ms = statistics.median(device_ms(b, 20))
+    res = b.results()
+    fields = ("peak_reserved", "peak_allocated", "final_reserved", "final_allocated",
+              "n_segments_final", "n_segments_peak")
+    mism = sum(int(res[i][f]) != g[f] for i, g in enumerate(gold["traces"]) for f in fields)
+    n2 = int(z["offsets"][-1])
+    out["c2"] = {"workload": "64 GPT-2 small training sequences (batch 1..64, seq 128, "
+                             "AdamW, 2 iterations) as one replay batch",
+                 "requests": n2, "ms": ms, "value": n2 / (ms / 1e3), "unit": "events/s",
+                 "reference_mismatches": mism, "timing": "CUDA events, median of 20"}
+    # C4
+    from c4_cases import c4_batch, c4_configs
+    zc = np.load(REPO / "tests" / "golden" / "c2_sequences.npz")
+    r3, o3 = synth.generate(42, first=9000)
+    reqs = np.concatenate([zc["reqs"], r3])
+    offs = np.concatenate([zc["offsets"], o3[1:] + zc["offsets"][-1]])
+    big, boffs, rec, cfg_of = c4_batch(reqs, offs, c4_configs())
+    b = DeviceBatch(big, boffs, rec, cfg_of, device=dev.index)
+    ms = min(device_ms(b, 3))
+    res = b.results()
+    ev4 = int(res["n_events_replayed"].sum())
+    out["c4"] = {"workload": "50 traces (8 GPT-2 sequences + 42 C3) x 69 allocator "
+                             "configs = 3450 replays, one batch",
+                 "requests": ev4, "ms": ms, "value": ev4 / (ms / 1e3), "unit": "events/s",
+                 "retry_passes": b.tier_counts(),
+                 "statuses": sorted(set(res["status"].tolist())),
+                 "parity": "tests/test_c4_sweep.py, tests/test_config_goldens.py "
+                           "(the reference's goldens on the grid)",
+                 "timing": "CUDA events, best of 3"}
+    # C5
+    bundle = synth_events.generate(357200, 2)
+    build_sequences([bundle], 2)  # warm (pool growth at this size)
+    torch.cuda.synchronize(dev)
+    t0 = time.perf_counter()
+    sb = build_sequences([bundle], 2)
+    torch.cuda.synchronize(dev)
+    t1 = time.perf_counter()
+    b = DeviceBatch(sb.d_reqs, sb.req_off, cfg_record(AllocatorConfig()), device=dev.index)
+    t2 = time.perf_counter()
+    b.launch(stream)
+    torch.cuda.synchronize(dev)
+    t3 = time.perf_counter()
+    res = b.results()
+    out["c5"] = {"workload": "one C5-style event-level trace, 357200 leaf layers, "
+                             "2 iterations", "events": len(bundle),
+                 "requests": int(sb.req_off[-1]),
+                 "analyze_build_sequence_s": t1 - t0,
+                 "replay_s": t3 - t2, "status": int(res[0]["status"]),
+                 "peak_reserved": int(res[0]["peak_reserved"]),
+                 "timing": "wall clock around synchronised calls (batched pipeline "
+                           "pm_pipeline_batch with B = 1; single-trace replay)"}
+    return out
 
 
 def cpu_baseline(reqs, offsets, cfg, stride: int, gpu_results=None):

@@ -293,14 +293,24 @@ __device__ __forceinline__ long long warp_incl_scan_ll(long long x) {
   return x;
 }
 
-// subtree sizes, one level at a time from the bottom
+// subtree sizes, one level at a time from the bottom.  One warp per node of
+// the level; a node with more than kBigNode children (a wrapper over
+// hundreds of thousands of layers) is handed to k_subtree_big, one CTA per
+// node (`big` collects them: big[0] = count, then the nodes).
+constexpr long long kBigNode = 2048;
 __global__ void k_subtree_level(const long long* lvl_nodes, long long m,
                                 const long long* child_order,
-                                const long long* off, long long* size) {
+                                const long long* off, long long* size,
+                                long long* big) {
   const long long w = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (w >= m) return;  // whole warp
   const long long v = lvl_nodes[w];
+  if (off[v + 2] - off[v + 1] > kBigNode) {
+    if (lane == 0)
+      big[1 + atomicAdd(reinterpret_cast<unsigned long long*>(big), 1ull)] = v;
+    return;
+  }
   long long s = 0;
   for (long long k = off[v + 1] + lane; k < off[v + 2]; k += 32)
     s += size[child_order[k]];
@@ -308,8 +318,56 @@ __global__ void k_subtree_level(const long long* lvl_nodes, long long m,
   if (lane == 0) size[v] = s + 1;
 }
 
+constexpr int kBigThreads = 512;
+__global__ void __launch_bounds__(kBigThreads)
+    k_subtree_big(const long long* big, const long long* child_order,
+                  const long long* off, long long* size) {
+  typedef cub::BlockReduce<long long, kBigThreads> BR;
+  __shared__ typename BR::TempStorage tmp;
+  const long long nbig = big[0];
+  for (long long i = blockIdx.x; i < nbig; i += gridDim.x) {
+    const long long v = big[1 + i];
+    long long s = 0;
+    for (long long k = off[v + 1] + threadIdx.x; k < off[v + 2]; k += kBigThreads)
+      s += size[child_order[k]];
+    s = BR(tmp).Sum(s);
+    if (threadIdx.x == 0) size[v] = s + 1;
+    __syncthreads();
+  }
+}
+
+// pre-order positions of the children of the big nodes of a level (and of
+// the synthetic root, big == nullptr): one CTA per node, 512 children per
+// step, a block-wide exclusive scan of their subtree sizes
+__global__ void __launch_bounds__(kBigThreads)
+    k_preorder_big(const long long* big, const long long* child_order,
+                   const long long* off, const long long* size, long long* pre) {
+  typedef cub::BlockScan<long long, kBigThreads> BS;
+  __shared__ typename BS::TempStorage tmp;
+  const long long nbig = big ? big[0] : 1;
+  for (long long i = blockIdx.x; i < nbig; i += gridDim.x) {
+    const long long v = big ? big[1 + i] : -1;
+    long long next = v >= 0 ? pre[v] + 1 : 0;
+    const long long b = off[v + 2];
+    for (long long base = off[v + 1]; base < b; base += kBigThreads) {
+      const long long k = base + threadIdx.x;
+      long long c = -1, sz = 0;
+      if (k < b) {
+        c = child_order[k];
+        sz = size[c];
+      }
+      long long ex, total;
+      BS(tmp).ExclusiveSum(sz, ex, total);
+      if (k < b) pre[c] = next + ex;
+      next += total;
+      __syncthreads();
+    }
+  }
+}
+
 // pre-order positions, one level at a time from the top: children of v
-// take consecutive ranges after pre[v] in (start, event) order
+// take consecutive ranges after pre[v] in (start, event) order (big nodes:
+// k_preorder_big)
 __global__ void k_preorder_level(const long long* lvl_nodes, long long m,
                                  const long long* child_order,
                                  const long long* off, const long long* size,
@@ -318,6 +376,7 @@ __global__ void k_preorder_level(const long long* lvl_nodes, long long m,
   const int lane = threadIdx.x & 31;
   if (w >= m) return;  // whole warp
   const long long v = lvl_nodes[w];  // -1: the synthetic root
+  if (off[v + 2] - off[v + 1] > kBigNode) return;
   long long next = v >= 0 ? pre[v] + 1 : 0;
   const long long b = off[v + 2];
   for (long long base = off[v + 1]; base < b; base += 32) {

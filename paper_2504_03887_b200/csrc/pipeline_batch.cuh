@@ -400,13 +400,30 @@ __global__ void k_pack_b(const RawReqB* raw, const long long* perm,
   if (out_raw) out_raw[i] = k - b0;
 }
 
-// phase breakdown (estimator.py:160-164): ALLOC bytes by role, per trace
+// phase breakdown (estimator.py:160-164): ALLOC bytes by role, per trace.
+// A CTA whose tile lies in one trace sums into 8 shared counters and adds
+// them once (a single trace would otherwise serialise millions of atomics
+// on seven addresses).
 __global__ void k_breakdown(const RawReqB* raw, long long n,
                             unsigned long long* bd) {
-  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const RawReqB r = raw[i];
-  if (r.kind == 0) atomicAdd(&bd[8 * r.tr + r.role], (unsigned long long)r.size);
+  __shared__ unsigned long long acc[8];
+  const long long t0 = (long long)blockIdx.x * kTile;
+  if (t0 >= n) return;
+  const long long t1 = t0 + kTile < n ? t0 + kTile : n;
+  const int ta = raw[t0].tr, tb = raw[t1 - 1].tr;
+  if (threadIdx.x < 8) acc[threadIdx.x] = 0ull;
+  __syncthreads();
+  for (long long i = t0 + threadIdx.x; i < t1; i += blockDim.x) {
+    const RawReqB r = raw[i];
+    if (r.kind != 0) continue;
+    if (ta == tb)
+      atomicAdd(&acc[r.role], (unsigned long long)r.size);
+    else
+      atomicAdd(&bd[8 * r.tr + r.role], (unsigned long long)r.size);
+  }
+  __syncthreads();
+  if (ta == tb && threadIdx.x < 8 && acc[threadIdx.x])
+    atomicAdd(&bd[8 * ta + threadIdx.x], acc[threadIdx.x]);
 }
 
 // ordered request columns for the single-trace API
@@ -451,9 +468,11 @@ __global__ void k_block_trace(const long long* b_inst, const int* itr,
   if (b < nb) trb[b] = itr[b_inst[b]];
 }
 
-__global__ void k_count_trace(const int* tr, long long n, long long* cnt) {
-  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (i < n) atomicAdd(reinterpret_cast<unsigned long long*>(&cnt[tr[i]]), 1ull);
+// first index of each trace in a trace-sorted column (off[B] = n)
+__global__ void k_trace_offsets(const int* tr, long long n, int B, long long* off) {
+  int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t > B) return;
+  off[t] = lower_bound_ll(tr, n, t);
 }
 
 }  // namespace pmp
@@ -602,21 +621,33 @@ int layer_tree_core(Arena& A, long long n, const long long* d_pid,
   std::vector<long long> h_lvl(maxd + 2);
   PM_TRY(download(h_lvl.data(), lvl, maxd + 2, s));
   PM_TRY(sync_check(s, "layer tree: levels"));
-  // subtree sizes bottom-up, pre-order positions top-down
+  // subtree sizes bottom-up, pre-order positions top-down; per level the
+  // nodes with more than kBigNode children go to the CTA-per-node kernels
+  // (big[d]: count, then nodes -- a level holds at most nl / kBigNode of them)
+  const long long bigcap = 1 + nl / pmp::kBigNode + 1;
+  long long* big = A.alloc<long long>((size_t)(maxd + 1) * bigcap);
+  PM_TRY(check_arena(A, "layer tree big nodes"));
+  cudaMemsetAsync(big, 0, sizeof(long long) * (size_t)(maxd + 1) * bigcap, s);
+  const unsigned big_grid = 148;
   for (int d = maxd; d >= 0; --d) {
     const long long a = h_lvl[d], b = h_lvl[d + 1];
-    if (b > a)
+    if (b > a) {
+      long long* bd = big + (size_t)d * bigcap;
       pmp::k_subtree_level<<<blocks_for(32 * (b - a)), 256, 0, s>>>(by_depth + a, b - a,
-                                                              ord, T->off, size);
+                                                              ord, T->off, size, bd);
+      pmp::k_subtree_big<<<big_grid, pmp::kBigThreads, 0, s>>>(bd, ord, T->off, size);
+    }
   }
-  const long long m1 = -1;
-  cudaMemcpyAsync(minus1, &m1, sizeof(long long), cudaMemcpyHostToDevice, s);
-  pmp::k_preorder_level<<<1, 32, 0, s>>>(minus1, 1, ord, T->off, size, pre);
+  (void)minus1;
+  pmp::k_preorder_big<<<1, pmp::kBigThreads, 0, s>>>(nullptr, ord, T->off, size, pre);
   for (int d = 0; d < maxd; ++d) {
     const long long a = h_lvl[d], b = h_lvl[d + 1];
-    if (b > a)
+    if (b > a) {
       pmp::k_preorder_level<<<blocks_for(32 * (b - a)), 256, 0, s>>>(by_depth + a, b - a,
                                                                ord, T->off, size, pre);
+      pmp::k_preorder_big<<<big_grid, pmp::kBigThreads, 0, s>>>(big + (size_t)d * bigcap, ord,
+                                                               T->off, size, pre);
+    }
   }
   // reachable nodes: depth >= 0, i.e. by_depth[h_lvl[0] ..]
   const long long r0 = h_lvl[0], nr = h_lvl[maxd + 1] - h_lvl[0];
@@ -790,7 +821,7 @@ int orch_core(Arena& A, const OrchIn& in, pm_req_t* packed, long long req_cap,
       PM_TRY(sort_pairs(A, keys, O->perm, n, bits_for(B)));
     }
     k_pack_b<<<blocks_for(n), 256, 0, s>>>(O->raw, O->perm, O->d_roff, n, packed, out_raw);
-    k_breakdown<<<blocks_for(n), 256, 0, s>>>(O->raw, n, O->bd);
+    k_breakdown<<<(unsigned)((n + kTile - 1) / kTile), 256, 0, s>>>(O->raw, n, O->bd);
   }
   return PM_SUCCESS;
 }
@@ -1119,23 +1150,23 @@ int pm_pipeline_batch(const pm_pipeline_batch_t* in, pm_req_t* reqs,
   // blocks back in their trace's own time; per-trace block offsets
   const long long nb = Bk.n;
   int* trb = A.alloc<int>(nb);
-  long long* bcnt = A.alloc<long long>(B + 1);
   long long* blk_off = A.alloc<long long>(B + 1);
   long long* b_alloc = A.alloc<long long>(nb);
   long long* b_free = A.alloc<long long>(nb);
   PM_TRY(check_arena(A, "pm_pipeline_batch blocks"));
-  cudaMemsetAsync(bcnt, 0, sizeof(long long) * (B + 1), s);
   if (nb > 0) {
+    // blocks are in instant order, i.e. trace-major: offsets by bisection
     k_block_trace<<<blocks_for(nb), 256, 0, s>>>(Bk.inst, tri, nb, trb);
-    k_count_trace<<<blocks_for(nb), 256, 0, s>>>(trb, nb, bcnt);
+    k_trace_offsets<<<blocks_for(B + 1), 256, 0, s>>>(trb, nb, B, blk_off);
     std::vector<long long> neg(B);
     for (int t = 0; t < B; ++t) neg[t] = -delta[t];
     long long* d_neg = A.upload(neg.data(), B);
     PM_TRY(check_arena(A, "pm_pipeline_batch blocks"));
     k_rebase<<<blocks_for(nb), 256, 0, s>>>(Bk.alloc, trb, d_neg, nb, INT64_MIN, b_alloc);
     k_rebase<<<blocks_for(nb), 256, 0, s>>>(Bk.free, trb, d_neg, nb, INT64_MIN, b_free);
+  } else {
+    cudaMemsetAsync(blk_off, 0, sizeof(long long) * (B + 1), s);
   }
-  PM_TRY(excl_sum(A, bcnt, blk_off, B + 1));
   std::vector<long long> h_blk_off(B + 1);
   std::vector<int> h_cyc(B);
   PM_TRY(download(h_blk_off.data(), blk_off, B + 1, s));
