@@ -560,11 +560,9 @@ __device__ __forceinline__ int best_fit(const NPool& P, const D& dir,
   if (dir.nb == 0) return -1;
   const int d = dir.find((u64)ru << 32);
   const int p = dir.phys(d);
-  // the whole bucket is loaded (empty slots hold stale entries, masked out)
   const bool in = (dir.mask(d) >> lane) & 1u;
-  const u64 kr = P.ka[p * kBucket + lane];
-  const u64 ln = P.ln[p * kBucket + lane];
-  const u64 ka = in ? kr : ~0ull;
+  const u64 ka = in ? P.ka[p * kBucket + lane] : ~0ull;
+  const u64 ln = in ? P.ln[p * kBucket + lane] : 0ull;
   PM_STAT(8);
   const bool el = in && hi(ka) >= ru && hi(ka) - ru < span;
   const int w = argmin_pk(el, ka);
@@ -579,8 +577,7 @@ __device__ __forceinline__ int best_fit(const NPool& P, const D& dir,
   if (d + 1 >= dir.nb) return -1;
   const int p2 = dir.phys(d + 1);
   const bool in2 = (dir.mask(d + 1) >> lane) & 1u;
-  const u64 kr2 = P.ka[p2 * kBucket + lane];
-  const u64 ka2 = in2 ? kr2 : ~0ull;
+  const u64 ka2 = in2 ? P.ka[p2 * kBucket + lane] : ~0ull;
   const int w2 = argmin_pk(in2, ka2);
   if (w2 >= 0) {
     const u64 kw = __shfl_sync(kFull, ka2, w2);
