@@ -47,6 +47,8 @@ def main():
         "warp_instructions_per_event": round(inst / events, 1),
         "smsp_issue_active_pct": round(num(get["smsp__issue_active.avg.pct_of_peak_sustained_active"][0]), 1),
         "warps_active_per_scheduler": round(num(get["smsp__warps_active.avg.per_cycle_active"][0]), 2),
+        "thread_inst_per_warp_inst": round(num(get["smsp__thread_inst_executed_per_inst_executed.ratio"][0]), 2)
+        if "smsp__thread_inst_executed_per_inst_executed.ratio" in get else None,
         "stall_pct": {s: round(100 * v / tot, 1) for s, v in
                       sorted(samples.items(), key=lambda x: -x[1]) if v / tot > 0.005},
     }

@@ -20,6 +20,7 @@ def main():
     ap.add_argument("--traces", type=int, default=600)
     ap.add_argument("--first", type=int, default=0)
     ap.add_argument("--launches", type=int, default=2)
+    ap.add_argument("--lib", default=None, help="an alternative build of the engine")
     args = ap.parse_args()
     import torch
     import __graft_entry__
@@ -27,6 +28,9 @@ def main():
     from paper_2504_03887_b200 import synth
     from paper_2504_03887_b200.allocator import AllocatorConfig, cfg_record
     from paper_2504_03887_b200.engine import DeviceBatch
+    if args.lib:
+        from paper_2504_03887_b200 import _native
+        _native._lib = _native.load_library(args.lib)
     reqs, offs = synth.generate(args.traces, first=args.first)
     batch = DeviceBatch(reqs, offs, cfg_record(AllocatorConfig()))
     for _ in range(args.launches):
