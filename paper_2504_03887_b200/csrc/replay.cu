@@ -168,6 +168,9 @@ int query_occupancy(Occupancy* out) {
     // when PM_REPLAY_WIDE selects the wide main pass)
     const int nw = o.narrow ? o.warps : kNarrowWarps;
     switch (nw) {
+      // 1: one warp per CTA (no bucket hand-off between warps): the
+      // configuration compute-sanitizer's racecheck can judge completely
+      case 1: rc = setup_narrow<1>(optin, cap, &o.buckets_n, &o.smem_n, &o.per_sm_n); break;
       case 12: rc = setup_narrow<12>(optin, cap, &o.buckets_n, &o.smem_n, &o.per_sm_n); break;
       case 20: rc = setup_narrow<20>(optin, cap, &o.buckets_n, &o.smem_n, &o.per_sm_n); break;
       case 24: rc = setup_narrow<24>(optin, cap, &o.buckets_n, &o.smem_n, &o.per_sm_n); break;
@@ -234,6 +237,7 @@ int query_occupancy(Occupancy* out) {
     {
       cudaFuncAttributes fa;
       const void* fns[] = {
+          (const void*)pmn::replay_narrow_kernel<1>,
           (const void*)pmn::replay_narrow_kernel<12>, (const void*)pmn::replay_narrow_kernel<16>,
           (const void*)pmn::replay_narrow_kernel<20>, (const void*)pmn::replay_narrow_kernel<24>,
           (const void*)pmn::replay_narrow_kernel<28>, (const void*)pmn::replay_narrow_kernel<32>,
@@ -401,6 +405,7 @@ int replay_batch_impl(const pm_req_t* reqs, const int64_t* trace_offsets,
       0, trace_order, n_traces, list_m1, occ.buckets, group_end, n_groups, ready)
   if (narrow) {
     switch (mwarps) {
+      case 1: PM_LAUNCH_NARROW(1); break;
       case 12: PM_LAUNCH_NARROW(12); break;
       case 20: PM_LAUNCH_NARROW(20); break;
       case 24: PM_LAUNCH_NARROW(24); break;
