@@ -15,9 +15,8 @@ every rank its own 10^4-trace sweep instead.
           that time.
   e2e     the same step through the C ABI with HOST buffers:
           pm_replay_host on pinned 16 B pm_req_t records (the documented ABI
-          record): the library packs them to 8-byte wire words on host threads
-          while the kernels replay the groups already packed, reading them
-          over PCIe in place, + D2H of the per-trace results.  `e2e_wire` is the engine's 8-byte wire path,
+          record; the kernel reads them over PCIe in place) + D2H of the
+          per-trace results.  `e2e_wire` is the engine's 8-byte wire path,
           pm_wire_pack (host threads) INSIDE the timed region +
           pm_replay_host_wire.
   roofline  HBM: 16 B of packed request read per replayed event
@@ -483,15 +482,12 @@ def main():
         "config": workload_config(args, world),
         "requests_per_step": int(all_events),
         "e2e": {"value": e2e_value, "unit": "events/s",
-                "h2d_bytes_per_step": int(total * 8 + offs.nbytes + cfg.nbytes),
+                "h2d_bytes_per_step": h2d16,
                 "d2h_bytes_per_step": int(res_host.nbytes),
                 "steps": e2e_steps,
-                "input_bytes_per_step": h2d16,
-                "api": "pm_replay_host (C ABI) on pinned host pm_req_t records "
-                       "(16 B each): host threads pack them to 8-byte wire words "
-                       "group by group while the kernels replay the groups already "
-                       "packed (read in place over PCIe), then D2H of the per-trace "
-                       "results; one synchronous call timed on the host"},
+                "api": "pm_replay_host (C ABI): pinned host pm_req_t records "
+                       "(16 B, read in place over PCIe), D2H of the per-trace "
+                       "results, synchronous call timed on the host"},
         "e2e_wire": {"value": e2e_wire, "unit": "events/s",
                      "h2d_bytes_per_step": int(total * 8 + offs.nbytes + cfg.nbytes),
                      "d2h_bytes_per_step": int(res_wire.nbytes),

@@ -525,246 +525,6 @@ int pm_replay_batch(const pm_req_t* reqs, const int64_t* trace_offsets,
 
 namespace {
 
-// ---- pm_replay_host on pinned pm_req_t: pack to wire words while replaying ----
-//
-// A large pinned pm_req_t batch is read over PCIe at 16 B per request, which
-// caps the host-buffer path near the link's bandwidth.  Here the host packs
-// the records into 8-byte wire words (the pm_wire_pack encoding) into a
-// pinned, device-mapped buffer WHILE the kernels run: the traces are cut into
-// G groups in the main pass's longest-first order, the main pass is launched
-// first and waits per trace for its group's flag, and host threads pack group
-// after group, each followed by a 4-byte DMA of a pinned "1" into the group's
-// device flag.  The kernel reads the words in place (zero copy).  A trace the
-// wire format cannot hold is packed as "unknown kind" words and replayed
-// again afterwards from its pm_req_t records (results patched in).
-
-int replay_host_impl(const void* src, size_t wb, const int64_t* trace_offsets,
-                     int32_t n_traces, const pm_cfg_t* cfgs, int32_t n_cfgs,
-                     const int32_t* cfg_of_trace, pm_result_t* results,
-                     int64_t* timeline, void* stream_);
-
-struct PinnedWire {
-  std::mutex mu;
-  uint64_t* host = nullptr;
-  const uint64_t* dev = nullptr;
-  size_t words = 0;
-};
-PinnedWire g_wire;
-
-int replay_host_packed(const pm_req_t* reqs, const int64_t* trace_offsets,
-                       int32_t n_traces, const pm_cfg_t* cfgs, int32_t n_cfgs,
-                       const int32_t* cfg_of_trace, pm_result_t* results,
-                       int64_t total, int64_t max_ev, void* stream_) {
-  std::lock_guard<std::mutex> lk(g_wire.mu);  // one packed call at a time
-  // (+2 words: the kernel's 16-byte-aligned bulk loads may read one word past
-  // the last trace)
-  if (g_wire.words < (size_t)total + 2) {
-    if (g_wire.host) cudaFreeHost(g_wire.host);
-    g_wire.host = nullptr;
-    g_wire.words = 0;
-    void* h = nullptr;
-    cudaError_t e = cudaHostAlloc(&h, 8 * ((size_t)total + 2),
-                                  cudaHostAllocMapped | cudaHostAllocPortable);
-    if (e != cudaSuccess) return cuda_fail(e, "cudaHostAlloc (wire)");
-    void* d = nullptr;
-    e = cudaHostGetDevicePointer(&d, h, 0);
-    if (e != cudaSuccess) {
-      cudaFreeHost(h);
-      return cuda_fail(e, "cudaHostGetDevicePointer (wire)");
-    }
-    g_wire.host = static_cast<uint64_t*>(h);
-    g_wire.dev = static_cast<const uint64_t*>(d);
-    g_wire.words = (size_t)total + 2;
-  }
-  uint64_t* words = g_wire.host;
-  // longest-first order and G groups of ~equal request counts (as the
-  // streamed upload of replay_host_impl)
-  int G = (int)std::min<int64_t>(64, std::max<int64_t>(1, total >> 22));
-  if (G > n_traces) G = n_traces;
-  std::vector<int32_t> order(n_traces);
-  for (int32_t i = 0; i < n_traces; ++i) order[i] = i;
-  std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) {
-    return trace_offsets[a + 1] - trace_offsets[a] >
-           trace_offsets[b + 1] - trace_offsets[b];
-  });
-  std::vector<unsigned> group_end(G);
-  {
-    int g = 0;
-    int64_t acc = 0;
-    for (int32_t i = 0; i < n_traces; ++i) {
-      acc += trace_offsets[order[i] + 1] - trace_offsets[order[i]];
-      while (g < G - 1 && acc * G >= total * (int64_t)(g + 1)) group_end[g++] = (unsigned)(i + 1);
-    }
-    while (g < G) group_end[g++] = (unsigned)n_traces;
-  }
-  const Layout L = layout_for(total, max_ev, n_traces);
-  cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
-  static unsigned* one = nullptr;  // pinned source of the group flags
-  {
-    static std::mutex mu;
-    std::lock_guard<std::mutex> g(mu);
-    if (!one) {
-      cudaError_t e = cudaHostAlloc((void**)&one, sizeof(unsigned), cudaHostAllocPortable);
-      if (e != cudaSuccess) return cuda_fail(e, "cudaHostAlloc");
-      *one = 1u;
-    }
-  }
-  const size_t b_exp = align_up(16 * (size_t)total, 256);  // wide-tier expansion
-  const size_t b_offs = align_up(8 * (size_t)(n_traces + 1), 256);
-  const size_t b_cfgs = align_up(sizeof(pm_cfg_t) * (size_t)n_cfgs, 256);
-  const size_t b_i32 = align_up(4 * (size_t)n_traces, 256);
-  const size_t b_res = align_up(sizeof(pm_result_t) * (size_t)n_traces, 256);
-  const size_t b_grp = align_up(8 * (size_t)G, 256);
-  const size_t bytes = b_exp + b_offs + b_cfgs + 2 * b_i32 + b_res + 2 * b_grp + L.total;
-  keep_pool_mapped();
-  cudaStream_t cs = nullptr;
-  cudaError_t e = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking);
-  if (e != cudaSuccess) return cuda_fail(e, "cudaStreamCreate");
-  void* dmem = nullptr;
-  e = cudaMallocAsync(&dmem, bytes, stream);
-  if (e != cudaSuccess) {
-    cudaStreamDestroy(cs);
-    return cuda_fail(e, "cudaMallocAsync");
-  }
-  char* p = static_cast<char*>(dmem);
-  pm_req_t* d_exp = reinterpret_cast<pm_req_t*>(p);
-  p += b_exp;
-  int64_t* d_offs = reinterpret_cast<int64_t*>(p);
-  p += b_offs;
-  pm_cfg_t* d_cfgs = reinterpret_cast<pm_cfg_t*>(p);
-  p += b_cfgs;
-  int32_t* d_cfgof = reinterpret_cast<int32_t*>(p);
-  p += b_i32;
-  int32_t* d_order = reinterpret_cast<int32_t*>(p);
-  p += b_i32;
-  pm_result_t* d_res = reinterpret_cast<pm_result_t*>(p);
-  p += b_res;
-  unsigned* d_gend = reinterpret_cast<unsigned*>(p);
-  p += b_grp;
-  unsigned* d_ready = reinterpret_cast<unsigned*>(p);
-  p += b_grp;
-  void* d_ws = p;
-  int rc = PM_SUCCESS;
-  std::vector<int32_t> bad;  // traces without a wire encoding
-  std::mutex bad_mu;
-  cudaEvent_t zeroed = nullptr;
-  cudaEventCreateWithFlags(&zeroed, cudaEventDisableTiming);
-  cudaMemcpyAsync(d_offs, trace_offsets, 8 * (size_t)(n_traces + 1), cudaMemcpyHostToDevice, stream);
-  cudaMemcpyAsync(d_cfgs, cfgs, sizeof(pm_cfg_t) * (size_t)n_cfgs, cudaMemcpyHostToDevice, stream);
-  if (cfg_of_trace)
-    cudaMemcpyAsync(d_cfgof, cfg_of_trace, 4 * (size_t)n_traces, cudaMemcpyHostToDevice, stream);
-  cudaMemcpyAsync(d_order, order.data(), 4 * (size_t)n_traces, cudaMemcpyHostToDevice, stream);
-  cudaMemcpyAsync(d_gend, group_end.data(), 4 * (size_t)G, cudaMemcpyHostToDevice, stream);
-  cudaMemsetAsync(d_ready, 0, 4 * (size_t)G, stream);
-  cudaEventRecord(zeroed, stream);
-  cudaStreamWaitEvent(cs, zeroed, 0);
-  e = cudaGetLastError();
-  if (e != cudaSuccess) rc = cuda_fail(e, "pm_replay_host (pack) setup");
-  if (rc == PM_SUCCESS)
-    rc = replay_batch_impl(d_exp, d_offs, n_traces, d_cfgs, cfg_of_trace ? d_cfgof : nullptr,
-                           d_order, d_res, nullptr, d_ws, L.total, total, max_ev, stream_,
-                           d_gend, G, d_ready, std::function<int()>(), g_wire.dev);
-  if (rc != PM_SUCCESS) {
-    cudaMemsetAsync(d_ready, 0xFF, 4 * (size_t)G, cs);  // release any waiter
-  } else {
-    // pack group after group on host threads; each group's flag follows it
-    unsigned hw = std::thread::hardware_concurrency();
-    const int nt = (int)std::max(1u, std::min(hw ? hw : 1u, 32u));
-    int32_t i0 = 0;
-    for (int g = 0; g < G; ++g) {
-      const int32_t i1 = (int32_t)group_end[g];
-      int64_t greq = 0;
-      for (int32_t i = i0; i < i1; ++i) greq += trace_offsets[order[i] + 1] - trace_offsets[order[i]];
-      auto work = [&](int w, int nw) {
-        // traces i0..i1 of the group, split by cumulative request count
-        int64_t acc = 0;
-        const int64_t lo = greq * w / nw, hi = greq * (w + 1) / nw;
-        for (int32_t i = i0; i < i1; ++i) {
-          const int32_t t = order[i];
-          const int64_t len = trace_offsets[t + 1] - trace_offsets[t];
-          const int64_t mid = acc + len / 2;  // a trace belongs to one worker
-          acc += len;
-          if (mid < lo || mid >= hi) {
-            if (!(len == 0 && w == 0 && acc == 0)) continue;
-          }
-          int64_t allocs = 0;
-          bool ok = true;
-          for (int64_t k = trace_offsets[t]; k < trace_offsets[t + 1]; ++k) {
-            const pm_req_t& r = reqs[k];
-            const uint32_t kind = r.kind_stream & 3u;
-            if (kind == PM_KIND_ALLOC && (r.kind_stream >> 2) == 0 && r.handle == allocs &&
-                r.size >= 1 && r.size < (int64_t)(1ll << 62)) {
-              words[k] = (uint64_t)r.size;
-              ++allocs;
-            } else if (kind == PM_KIND_FREE && r.handle >= 0) {
-              words[k] = PM_WIRE_FREE | (uint64_t)(uint32_t)r.handle;
-            } else {
-              ok = false;
-              break;
-            }
-          }
-          if (!ok) {
-            // an "unknown kind" trace for the kernel; replayed again below
-            for (int64_t k = trace_offsets[t]; k < trace_offsets[t + 1]; ++k)
-              words[k] = 3ull << 62;
-            std::lock_guard<std::mutex> b(bad_mu);
-            bad.push_back(t);
-          }
-        }
-      };
-      const int nw = (int)std::min<int64_t>(nt, std::max<int64_t>(1, greq >> 16));
-      if (nw <= 1) {
-        work(0, 1);
-      } else {
-        std::vector<std::thread> th;
-        for (int w = 0; w < nw; ++w) th.emplace_back(work, w, nw);
-        for (auto& x : th) x.join();
-      }
-      cudaError_t ce = cudaMemcpyAsync(d_ready + g, one, sizeof(unsigned),
-                                       cudaMemcpyHostToDevice, cs);
-      if (ce != cudaSuccess) {
-        cudaMemsetAsync(d_ready, 0xFF, 4 * (size_t)G, cs);
-        rc = cuda_fail(ce, "H2D flag");
-        break;
-      }
-      i0 = i1;
-    }
-  }
-  if (rc == PM_SUCCESS) {
-    e = cudaMemcpyAsync(results, d_res, sizeof(pm_result_t) * (size_t)n_traces,
-                        cudaMemcpyDeviceToHost, stream);
-    if (e != cudaSuccess) rc = cuda_fail(e, "D2H results");
-  }
-  {
-    cudaError_t e2 = cudaStreamSynchronize(cs);
-    if (rc == PM_SUCCESS && e2 != cudaSuccess) rc = cuda_fail(e2, "flag stream");
-  }
-  cudaFreeAsync(dmem, stream);
-  e = cudaStreamSynchronize(stream);
-  if (rc == PM_SUCCESS && e != cudaSuccess) rc = cuda_fail(e, "cudaStreamSynchronize");
-  cudaEventDestroy(zeroed);
-  cudaStreamDestroy(cs);
-  if (rc != PM_SUCCESS || bad.empty()) return rc;
-  // traces the wire format cannot hold: replay them from their records
-  std::sort(bad.begin(), bad.end());
-  std::vector<int64_t> offs(bad.size() + 1, 0);
-  for (size_t k = 0; k < bad.size(); ++k)
-    offs[k + 1] = offs[k] + trace_offsets[bad[k] + 1] - trace_offsets[bad[k]];
-  std::vector<pm_req_t> sub((size_t)std::max<int64_t>(offs.back(), 1));
-  std::vector<int32_t> sub_cfg(bad.size());
-  for (size_t k = 0; k < bad.size(); ++k) {
-    std::copy(reqs + trace_offsets[bad[k]], reqs + trace_offsets[bad[k] + 1],
-              sub.begin() + offs[k]);
-    sub_cfg[k] = cfg_of_trace ? cfg_of_trace[bad[k]] : 0;
-  }
-  std::vector<pm_result_t> sub_res(bad.size());
-  rc = replay_host_impl(sub.data(), 16, offs.data(), (int32_t)bad.size(), cfgs, n_cfgs,
-                        sub_cfg.data(), sub_res.data(), nullptr, stream_);
-  if (rc != PM_SUCCESS) return rc;
-  for (size_t k = 0; k < bad.size(); ++k) results[bad[k]] = sub_res[k];
-  return PM_SUCCESS;
-}
-
 // pm_replay_host / pm_replay_host_wire: `src` holds pm_req_t records
 // (wb = 16) or wire words (wb = 8).  Wire words are replayed by the narrow
 // main pass directly; d_reqs then only receives the pm_req_t expansion of
@@ -849,16 +609,6 @@ int replay_host_impl(const void* src, size_t wb, const int64_t* trace_offsets,
       pinned && !(copy_env && atoi(copy_env) != 0) &&
       cudaHostGetDevicePointer(&mapped, const_cast<char*>(reqs), 0) == cudaSuccess;
   cudaGetLastError();
-  {
-    // large pinned pm_req_t batches: pack to wire words on host threads while
-    // the kernels replay (half the PCIe bytes); PM_HOST_PACK=0 disables
-    const char* pack_env = getenv("PM_HOST_PACK");
-    if (!wire && zero_copy && timeline == nullptr && total >= (1 << 20) &&
-        !(pack_env && atoi(pack_env) == 0))
-      return replay_host_packed(reinterpret_cast<const pm_req_t*>(reqs), trace_offsets,
-                                n_traces, cfgs, n_cfgs, cfg_of_trace, results, total,
-                                max_ev, stream_);
-  }
   // d_reqs: staged pm_req_t, or (wire) the expansion of escalated traces
   const size_t b_reqs = (zero_copy && !wire)
                             ? 256
