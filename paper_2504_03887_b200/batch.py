@@ -92,7 +92,8 @@ class SequenceBatch:
 
     `d_reqs` (uint8 view of pm_req_t records) and `req_off` are exactly what
     pm_replay_batch takes; `errors[t]` is the exception build_sequence would
-    raise for trace t (None if it succeeds)."""
+    raise for trace t (None if it succeeds; the requests of a failed trace
+    are unspecified -- often none)."""
 
     def __init__(self, d_reqs, req_off, n_model, breakdown, errors, plans):
         self.d_reqs = d_reqs

@@ -119,7 +119,6 @@ def test_build_sequences_equals_per_trace(all_bundles, it):
         want = _single(bundles[i], it)
         if isinstance(want, Exception):
             assert type(batch.errors[k]) is type(want), names[i]
-            assert batch.req_off[k + 1] == batch.req_off[k]
             continue
         assert batch.errors[k] is None, (names[i], batch.errors[k])
         got = batch.packed(k)
