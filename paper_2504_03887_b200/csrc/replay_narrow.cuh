@@ -1223,9 +1223,10 @@ __device__ __forceinline__ void replay_trace(
     uint4 ev_next = reinterpret_cast<const uint4*>(cb)[j0];
     for (int j = j0; j < cnt; ++j) {
       // the next request's word is loaded before this one's dependent chain
-      // (slot 32 lies inside the staging area: read, never used)
+      // (clamped to the chunk's own buffer: slot 32 would be the other
+      // buffer, which the prefetch's bulk copy may be writing)
       const uint4 ev = ev_next;
-      ev_next = reinterpret_cast<const uint4*>(cb)[j + 1];
+      ev_next = reinterpret_cast<const uint4*>(cb)[min(j + 1, 31)];
       bool handoff = false;  // an entry was parked: hand off after this request
       const int hj = (int)ev.y;
       const unsigned kind = ev.z & 3u;
