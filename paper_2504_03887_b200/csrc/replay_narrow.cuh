@@ -291,50 +291,17 @@ struct __align__(16) NWarpState {
 constexpr size_t kWarpStageBytes =
     (2 * 32 * 16 + 32 * 16 + 16 + sizeof(NWarpState) + 15) / 16 * 16;
 
-// ---- predicated stores --------------------------------------------------------
-//
-// A lane-conditional store written as `if (lane == k) *p = v` becomes a
-// branch around the store, and the compiler brackets it with a convergence
-// region (BSSY / BSYNC) and then guards every later collective of the request
-// with a divergence check.  These emit one predicated store instead:
-// straight-line code, the warp provably converged throughout.
-
-__device__ __forceinline__ void st_shared_if(bool p, u32* a, u32 v) {
-  asm volatile("{ .reg .pred q; setp.ne.u32 q, %0, 0; @q st.shared.u32 [%1], %2; }"
-               ::"r"((u32)p), "r"((u32)__cvta_generic_to_shared(a)), "r"(v)
-               : "memory");
-}
-__device__ __forceinline__ void st_shared_if(bool p, uint4* a, uint4 v) {
-  asm volatile("{ .reg .pred q; setp.ne.u32 q, %0, 0;"
-               " @q st.shared.v4.u32 [%1], {%2, %3, %4, %5}; }"
-               ::"r"((u32)p), "r"((u32)__cvta_generic_to_shared(a)), "r"(v.x), "r"(v.y),
-               "r"(v.z), "r"(v.w)
-               : "memory");
-}
-__device__ __forceinline__ void st_global_if(bool p, u32* a, u32 v) {
-  asm volatile("{ .reg .pred q; setp.ne.u32 q, %0, 0; @q st.global.u32 [%1], %2; }"
-               ::"r"((u32)p), "l"(a), "r"(v)
-               : "memory");
-}
-__device__ __forceinline__ void st_global_if(bool p, uint4* a, uint4 v) {
-  asm volatile("{ .reg .pred q; setp.ne.u32 q, %0, 0;"
-               " @q st.global.v4.u32 [%1], {%2, %3, %4, %5}; }"
-               ::"r"((u32)p), "l"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
-               : "memory");
-}
-__device__ __forceinline__ void st_global_if(bool p, longlong2* a, longlong2 v) {
-  asm volatile("{ .reg .pred q; setp.ne.u32 q, %0, 0;"
-               " @q st.global.v2.s64 [%1], {%2, %3}; }"
-               ::"r"((u32)p), "l"(a), "l"(v.x), "l"(v.y)
-               : "memory");
-}
-
 // ---- record refs (global store + staged mirror) ---------------------------
 
 __device__ __forceinline__ void set_link(const NRecs& rec, uint4* st, int hcmp,
                                          int lane, u32 g, int right, u32 val) {
-  st_global_if(lane == 0, rec.word(g, 2 + right), val);
-  st_shared_if(hcmp == (int)g, reinterpret_cast<u32*>(st + lane) + 2 + right, val);
+  if (lane == 0) *rec.word(g, 2 + right) = val;
+  if (hcmp == (int)g) {
+    if (right)
+      st[lane].w = val;
+    else
+      st[lane].z = val;
+  }
 }
 
 __device__ __forceinline__ void relink_lanes(const NRecs& rec, uint4* st,
@@ -1400,12 +1367,14 @@ __device__ __forceinline__ void replay_trace(
           if (is_alloc) {
             c.allocated += (long long)out_s << s;
             c.peak_allocated = max(c.peak_allocated, c.allocated);
-            const uint4 o = make_uint4(out_a, out_s, out_L, out_R);
-            st_shared_if(lane == j, st + j, o);
-            st_global_if(lane == j, myrec, o);
-          } else {
-            st_shared_if(lane == j, reinterpret_cast<u32*>(st + j) + 1, kFreedU);
-            st_global_if(lane == j, reinterpret_cast<u32*>(myrec) + 1, kFreedU);
+            if (lane == j) {
+              const uint4 o = make_uint4(out_a, out_s, out_L, out_R);
+              st[j] = o;
+              *myrec = o;
+            }
+          } else if (lane == j) {
+            st[j].y = kFreedU;
+            reinterpret_cast<u32*>(myrec)[1] = kFreedU;
           }
         }
       }
@@ -1430,8 +1399,9 @@ __device__ __forceinline__ void replay_trace(
         stop = cbase + j;
         break;
       }
-      st_global_if(tl != nullptr && lane == j, tl + cbase + j,
-                   make_longlong2(c.reserved, c.allocated));
+      if (tl != nullptr && lane == j)
+        tl[cbase + j] =
+            make_longlong2(c.reserved, c.allocated);
       __syncwarp();
       if (handoff) {
         // the request is complete; continue at the next one in the next pass
