@@ -169,9 +169,34 @@ typedef struct {
  * n_model (model-load requests), breakdown (nullable, [n_traces x 8]:
  * ALLOC bytes by role code 0 unclassified, 1 model, 2 batch, 3 gradient,
  * 4 optimizer_state, 5 temporary, 6 retained -- estimator.py:160-164). */
+/* Optional per-trace views (all HOST, caller-allocated; pass NULL to skip):
+ * the ordered request columns of every trace, concatenated like `reqs`
+ * (capacity req_cap): raw index within the trace, kind (0 alloc, 1 free),
+ * size, virtual_ts, tag (0 model / 1 batch / 2 block / 3 clone), a, b (the
+ * block-id parts: model i | batch it, j | block id | clone c, id), role;
+ * every block's final role and free time after orchestration (capacity
+ * fb_cap >= all traces' blocks; build_sequence mutates the analyzed blocks
+ * so, orchestration.py:222-223,197) and the per-trace block offsets
+ * blk_off[n_traces + 1]. */
+typedef struct {
+  int64_t* o_raw;
+  int32_t* o_kind;
+  int64_t* o_size;
+  int64_t* o_vts;
+  int32_t* o_tag;
+  int64_t* o_a;
+  int64_t* o_b;
+  int32_t* o_role;
+  int32_t* fb_role;
+  int64_t* fb_free;
+  int64_t fb_cap;
+  int64_t* blk_off;
+} pm_pipeline_views_t;
+
 int pm_pipeline_batch(const pm_pipeline_batch_t* in, pm_req_t* reqs,
                       int64_t req_cap, int64_t* req_off, int32_t* status,
-                      int64_t* n_model, int64_t* breakdown, void* stream);
+                      int64_t* n_model, int64_t* breakdown,
+                      pm_pipeline_views_t* views, void* stream);
 
 #ifdef __cplusplus
 }

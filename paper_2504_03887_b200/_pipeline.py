@@ -300,22 +300,50 @@ class PipelineBatch(ctypes.Structure):
     _fields_ = _BATCH_FIELDS
 
 
+class PipelineViews(ctypes.Structure):
+    """pm_pipeline_views_t (include/peakmem_pipeline.h)."""
+
+    _fields_ = [*[(f, ctypes.c_void_p) for f in (
+        "o_raw", "o_kind", "o_size", "o_vts", "o_tag", "o_a", "o_b", "o_role",
+        "fb_role", "fb_free")], ("fb_cap", ctypes.c_int64), ("blk_off", ctypes.c_void_p)]
+
+
 def pipeline_batch(desc: PipelineBatch, d_reqs_ptr: int, req_cap: int,
-                   n_traces: int):
+                   n_traces: int, fb_cap: int | None = None):
     """Run pm_pipeline_batch; the host arrays `desc` points at must stay
-    alive for the call.  Returns (req_off, status, n_model, breakdown)."""
+    alive for the call.  Returns (req_off, status, n_model, breakdown,
+    views) -- views (a dict of host arrays) only when fb_cap is given."""
     lib = load()
     _native.require_device()
     req_off = np.zeros(n_traces + 1, np.int64)
     status = np.zeros(n_traces, np.int32)
     n_model = np.zeros(n_traces, np.int64)
     breakdown = np.zeros((n_traces, 8), np.int64)
+    views = None
+    vdesc = None
+    if fb_cap is not None:
+        cap = max(req_cap, 1)
+        views = {"raw": np.empty(cap, np.int64), "kind": np.empty(cap, np.int32),
+                 "size": np.empty(cap, np.int64), "vts": np.empty(cap, np.int64),
+                 "tag": np.empty(cap, np.int32), "a": np.empty(cap, np.int64),
+                 "b": np.empty(cap, np.int64), "role": np.empty(cap, np.int32),
+                 "fb_role": np.empty(max(fb_cap, 1), np.int32),
+                 "fb_free": np.empty(max(fb_cap, 1), np.int64),
+                 "blk_off": np.zeros(n_traces + 1, np.int64)}
+        vdesc = PipelineViews()
+        for f in ("raw", "kind", "size", "vts", "tag", "a", "b", "role"):
+            setattr(vdesc, "o_" + f, views[f].ctypes.data)
+        vdesc.fb_role = views["fb_role"].ctypes.data
+        vdesc.fb_free = views["fb_free"].ctypes.data
+        vdesc.fb_cap = max(fb_cap, 1)
+        vdesc.blk_off = views["blk_off"].ctypes.data
     rc = lib.pm_pipeline_batch(ctypes.byref(desc), ctypes.c_void_p(d_reqs_ptr),
                                ctypes.c_int64(req_cap), _p(req_off), _p(status),
                                _p(n_model), _p(breakdown),
+                               ctypes.byref(vdesc) if vdesc is not None else None,
                                ctypes.c_void_p(_stream()))
     if rc == PM_ERR_WORKSPACE_TOO_SMALL:
         raise MemoryError(f"pm_pipeline_batch: {int(req_off[-1])} requests > "
                           f"capacity {req_cap}")
     _check(rc, lib)
-    return req_off, status, n_model, breakdown
+    return req_off, status, n_model, breakdown, views

@@ -121,9 +121,12 @@ class SequenceBatch:
         return self.d_reqs[a * rs:b * rs].cpu().numpy().view(_native.REQ_DTYPE).copy()
 
 
-def build_sequences(bundles, iterations: int = 2, device: int = 0) -> SequenceBatch:
+def build_sequences(bundles, iterations: int = 2, device: int = 0,
+                    views: bool = False) -> SequenceBatch:
     """orchestration.build_sequence(orchestration.analyze(b), iterations) for
-    every bundle, in one pm_pipeline_batch call."""
+    every bundle, in one pm_pipeline_batch call.  With views, the ordered
+    request columns and the blocks' final roles / frees come back too
+    (`SequenceBatch.views`)."""
     import torch
 
     _native.require_device()
@@ -228,8 +231,9 @@ def build_sequences(bundles, iterations: int = 2, device: int = 0) -> SequenceBa
     cap = int((counts["in"] * (3 + 2 * clones.astype(np.int64)) + bat_counts).sum()) + 16
     rs = _native.REQ_DTYPE.itemsize
     d_reqs = torch.empty(cap * rs, dtype=torch.uint8, device=dev)
-    req_off, status, n_model, bd = _pipeline.pipeline_batch(
-        desc, d_reqs.data_ptr(), cap, B)
+    req_off, status, n_model, bd, vw = _pipeline.pipeline_batch(
+        desc, d_reqs.data_ptr(), cap, B,
+        fb_cap=int(counts["in"].sum()) if views else None)
     del d, h  # the call synchronised its stream: the upload is consumed
     errors: list[BaseException | None] = []
     for t, tr in enumerate(traces):
@@ -246,8 +250,9 @@ def build_sequences(bundles, iterations: int = 2, device: int = 0) -> SequenceBa
             errors.append(RuntimeError(f"pm_pipeline_batch: trace {t} status {st}"))
         else:
             errors.append(None)
-    return SequenceBatch(d_reqs, req_off, n_model, bd, errors,
-                         [t.plan for t in traces])
+    sb = SequenceBatch(d_reqs, req_off, n_model, bd, errors, [t.plan for t in traces])
+    sb.views = vw
+    return sb
 
 
 __all__ = ["SequenceBatch", "build_sequences"]

@@ -139,10 +139,18 @@ class AnalyzedTrace:
         self.bundle = bundle
         self.markers = markers
         self._tree = tree_cols
-        self._link = link
+        self._link_data = link  # None until a view needs it
         self._ops = op_idx
         self._objects = None
         self._final = None  # (roles, frees) of the last build_sequence
+
+    @property
+    def _link(self):
+        """pm_link's columnar result, computed on first use (the object
+        views need it; build_sequence alone runs the batched pipeline)."""
+        if self._link_data is None:
+            self._link_data = _link_columns(self.bundle, self._tree, self._ops)
+        return self._link_data
 
     def _materialise(self):
         if self._objects is None:
@@ -188,19 +196,27 @@ class AnalyzedTrace:
                       key=lambda m: m.iteration_index)
 
 
-def analyze(bundle: TraceBundle) -> AnalyzedTrace:
-    """Build every structural view and link them (orchestration.py:107-116)."""
-    tree = LayerTreeColumns(bundle)
-    ops = bundle.indices(EventCategory.CPU_OP)
+def _link_columns(bundle: TraceBundle, tree, ops):
     inst = bundle.indices(EventCategory.CPU_INSTANT_EVENT)
-    markers = extract_markers(bundle.by_category(EventCategory.USER_ANNOTATION))
     seq = bundle.ints["sequence_number"][ops]
     seq = np.where(seq == NONE, -1, seq)
-    lk = _pipeline.link(bundle.start[ops], bundle.end[ops], seq,
-                        bundle.start[inst], bundle.ints["addr"][inst],
-                        bundle.ints["nbytes"][inst], tree.leaf_start,
-                        tree.leaf_end)
-    return AnalyzedTrace(bundle, tree, markers, lk, ops)
+    return _pipeline.link(bundle.start[ops], bundle.end[ops], seq,
+                          bundle.start[inst], bundle.ints["addr"][inst],
+                          bundle.ints["nbytes"][inst], tree.leaf_start,
+                          tree.leaf_end)
+
+
+def analyze(bundle: TraceBundle) -> AnalyzedTrace:
+    """Build every structural view and link them (orchestration.py:107-116).
+
+    The layer tree (CyclicParentLink) and the markers (NoIterationMarkers)
+    are built here, in the reference's order; the operator / block link is
+    computed when a view needs it -- build_sequence on its own takes the
+    batched device pipeline, which links on the device without a round trip."""
+    tree = LayerTreeColumns(bundle)
+    ops = bundle.indices(EventCategory.CPU_OP)
+    markers = extract_markers(bundle.by_category(EventCategory.USER_ANNOTATION))
+    return AnalyzedTrace(bundle, tree, markers, None, ops)
 
 
 def _block_id(tag: int, a: int, b: int):
@@ -293,6 +309,8 @@ def build_sequence(analyzed: AnalyzedTrace, iterations: int = 2,
                    ) -> RequestSequence:
     """Assemble the replayable request sequence (orchestration.py:237-399)."""
     plan = plan_sequence(analyzed.markers, analyzed.bundle.metadata, iterations)
+    if analyzed._link_data is None:
+        return _build_batched(analyzed, plan, iterations)
     lk = analyzed._link
     nb = int(lk.n_blocks)
     role_codes = lk.b_role if nb else np.zeros(0, np.int32)
@@ -313,6 +331,27 @@ def build_sequence(analyzed: AnalyzedTrace, iterations: int = 2,
               "vts": o.vts, "tag": o.tag, "a": o.a, "b": o.b, "role": o.role,
               "raw": o.raw, "batch_ids": plan.batch_ids}
     return RequestSequence(iteration_boundaries=plan.boundaries, packed=o.packed,
+                           arrays=arrays)
+
+
+def _build_batched(analyzed: AnalyzedTrace, plan, iterations: int) -> RequestSequence:
+    """build_sequence through pm_pipeline_batch (B = 1) with its views:
+    link, orchestration and the total order on the device in one call."""
+    from .batch import build_sequences
+    sb = build_sequences([analyzed.bundle], iterations, views=True)
+    if sb.errors[0] is not None:
+        raise sb.errors[0]
+    v = sb.views
+    n = int(sb.req_off[1])
+    nb = int(v["blk_off"][1])
+    analyzed._final = (v["fb_role"][:nb].copy(), v["fb_free"][:nb].copy())
+    if analyzed._objects is not None:
+        analyzed._apply_final()
+    arrays = {"n": n, "n_model": int(sb.n_model[0]),
+              **{f: v[f][:n].copy() for f in ("kind", "size", "vts", "tag", "a", "b",
+                                                "role", "raw")},
+              "batch_ids": plan.batch_ids}
+    return RequestSequence(iteration_boundaries=plan.boundaries, packed=sb.packed(0),
                            arrays=arrays)
 
 
