@@ -157,3 +157,27 @@ def test_estimate_many_validate_flag(all_bundles):
     got = api.PeakMemoryEstimator(validate=True).estimate_many([bundles[i] for i in pick])
     for i, g in zip(pick, got):
         assert g.canonical_json() == wants[i]["report_default"], names[i]
+
+
+@pytest.mark.parametrize("it", [1, 2, 3])
+def test_lazy_build_sequence_equals_viewed_path(all_bundles, it):
+    """build_sequence on an analyzed trace whose views were never asked for
+    (pm_pipeline_batch with views) == the per-stage path (pm_link +
+    pm_orchestrate, taken once a view exists): the request sequence, its
+    phase tags and boundaries, and the analyzed blocks mutated in place."""
+    names, bundles, _ = all_bundles
+    for name, b in zip(names, bundles):
+        lazy = api.analyze(b)
+        viewed = api.analyze(b)
+        _ = viewed.blocks  # materialise: the per-stage path
+        try:
+            s_viewed = api.build_sequence(viewed, iterations=it)
+        except Exception as exc:  # noqa: BLE001
+            with pytest.raises(type(exc)):
+                api.build_sequence(lazy, iterations=it)
+            continue
+        s_lazy = api.build_sequence(lazy, iterations=it)
+        assert s_lazy.to_json_dict() == s_viewed.to_json_dict(), name
+        assert (s_lazy.packed == s_viewed.packed).all(), name
+        assert [(x.block_id, x.free_time, x.role) for x in lazy.blocks] == \
+            [(x.block_id, x.free_time, x.role) for x in viewed.blocks], name
