@@ -169,7 +169,9 @@ typedef struct {
  * n_model (model-load requests), breakdown (nullable, [n_traces x 8]:
  * ALLOC bytes by role code 0 unclassified, 1 model, 2 batch, 3 gradient,
  * 4 optimizer_state, 5 temporary, 6 retained -- estimator.py:160-164). */
-/* Optional per-trace views (all HOST, caller-allocated; pass NULL to skip):
+/* Optional per-trace views (caller-allocated DEVICE buffers except blk_off,
+ * a HOST array; pass NULL to skip) -- left on the device so a caller reads
+ * them only if it needs them:
  * the ordered request columns of every trace, concatenated like `reqs`
  * (capacity req_cap): raw index within the trace, kind (0 alloc, 1 free),
  * size, virtual_ts, tag (0 model / 1 batch / 2 block / 3 clone), a, b (the

@@ -322,19 +322,22 @@ def pipeline_batch(desc: PipelineBatch, d_reqs_ptr: int, req_cap: int,
     views = None
     vdesc = None
     if fb_cap is not None:
+        # device buffers: read back only when a view is asked for
+        import torch
+        dev = torch.device("cuda", torch.cuda.current_device())
         cap = max(req_cap, 1)
-        views = {"raw": np.empty(cap, np.int64), "kind": np.empty(cap, np.int32),
-                 "size": np.empty(cap, np.int64), "vts": np.empty(cap, np.int64),
-                 "tag": np.empty(cap, np.int32), "a": np.empty(cap, np.int64),
-                 "b": np.empty(cap, np.int64), "role": np.empty(cap, np.int32),
-                 "fb_role": np.empty(max(fb_cap, 1), np.int32),
-                 "fb_free": np.empty(max(fb_cap, 1), np.int64),
-                 "blk_off": np.zeros(n_traces + 1, np.int64)}
+        i64, i32 = torch.int64, torch.int32
+        views = {f: torch.empty(cap, dtype=dt, device=dev) for f, dt in (
+            ("raw", i64), ("kind", i32), ("size", i64), ("vts", i64), ("tag", i32),
+            ("a", i64), ("b", i64), ("role", i32))}
+        views["fb_role"] = torch.empty(max(fb_cap, 1), dtype=i32, device=dev)
+        views["fb_free"] = torch.empty(max(fb_cap, 1), dtype=i64, device=dev)
+        views["blk_off"] = np.zeros(n_traces + 1, np.int64)
         vdesc = PipelineViews()
         for f in ("raw", "kind", "size", "vts", "tag", "a", "b", "role"):
-            setattr(vdesc, "o_" + f, views[f].ctypes.data)
-        vdesc.fb_role = views["fb_role"].ctypes.data
-        vdesc.fb_free = views["fb_free"].ctypes.data
+            setattr(vdesc, "o_" + f, views[f].data_ptr())
+        vdesc.fb_role = views["fb_role"].data_ptr()
+        vdesc.fb_free = views["fb_free"].data_ptr()
         vdesc.fb_cap = max(fb_cap, 1)
         vdesc.blk_off = views["blk_off"].ctypes.data
     rc = lib.pm_pipeline_batch(ctypes.byref(desc), ctypes.c_void_p(d_reqs_ptr),

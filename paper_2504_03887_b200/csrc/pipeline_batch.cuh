@@ -1215,37 +1215,25 @@ int pm_pipeline_batch(const pm_pipeline_batch_t* in, pm_req_t* reqs,
   oi.bat_j = A.upload((const long long*)in->bat_j, bo[B]);
   PM_TRY(check_arena(A, "pm_pipeline_batch params"));
   OrchOut O;
-  long long* d_oraw = views ? A.alloc<long long>(req_cap) : nullptr;
-  PM_TRY(check_arena(A, "pm_pipeline_batch views"));
+  long long* d_oraw = views ? (long long*)views->o_raw : nullptr;
   int rc = orch_core(A, oi, reqs, req_cap, d_oraw, &O);
   for (int t = 0; t <= B; ++t) req_off[t] = O.roff.empty() ? 0 : O.roff[t];
   if (rc) return rc;
   if (views) {
-    // the per-trace views of build_sequence: the ordered request columns
-    // and every block's final role / lifetime (orchestration.py:222-223,197)
+    // the per-trace views of build_sequence, written to the caller's DEVICE
+    // buffers: the ordered request columns and every block's final role /
+    // lifetime (orchestration.py:222-223,197)
     if (nb > views->fb_cap) return perr(PM_ERR_WORKSPACE_TOO_SMALL, "pm_pipeline_batch: fb_cap");
     const long long n = O.n;
-    int32_t* d_kind = A.alloc<int32_t>(n);
-    long long* d_size = A.alloc<long long>(n);
-    long long* d_vts = A.alloc<long long>(n);
-    int32_t* d_tag = A.alloc<int32_t>(n);
-    long long* d_a = A.alloc<long long>(n);
-    long long* d_b = A.alloc<long long>(n);
-    int32_t* d_role = A.alloc<int32_t>(n);
-    PM_TRY(check_arena(A, "pm_pipeline_batch views"));
     if (n > 0)
-      k_unpack_ordered<<<blocks_for(n), 256, 0, s>>>(O.raw, O.perm, n, d_kind, d_size, d_vts,
-                                                     d_tag, d_a, d_b, d_role);
-    PM_TRY(download(views->o_raw, (const int64_t*)d_oraw, n, s));
-    PM_TRY(download(views->o_kind, d_kind, n, s));
-    PM_TRY(download(views->o_size, (const int64_t*)d_size, n, s));
-    PM_TRY(download(views->o_vts, (const int64_t*)d_vts, n, s));
-    PM_TRY(download(views->o_tag, d_tag, n, s));
-    PM_TRY(download(views->o_a, (const int64_t*)d_a, n, s));
-    PM_TRY(download(views->o_b, (const int64_t*)d_b, n, s));
-    PM_TRY(download(views->o_role, d_role, n, s));
-    PM_TRY(download(views->fb_role, (const int32_t*)O.role, nb, s));
-    PM_TRY(download(views->fb_free, (const int64_t*)O.free_out, nb, s));
+      k_unpack_ordered<<<blocks_for(n), 256, 0, s>>>(
+          O.raw, O.perm, n, views->o_kind, (long long*)views->o_size,
+          (long long*)views->o_vts, views->o_tag, (long long*)views->o_a,
+          (long long*)views->o_b, views->o_role);
+    if (nb > 0) {
+      cudaMemcpyAsync(views->fb_role, O.role, sizeof(int32_t) * nb, cudaMemcpyDeviceToDevice, s);
+      cudaMemcpyAsync(views->fb_free, O.free_out, sizeof(int64_t) * nb, cudaMemcpyDeviceToDevice, s);
+    }
     for (int t = 0; t <= B; ++t) views->blk_off[t] = h_blk_off[t];
   }
   std::vector<unsigned long long> h_bd(8 * (size_t)B);

@@ -59,8 +59,23 @@ class RequestSequence:
         self._requests = requests
         self.iteration_boundaries = list(iteration_boundaries or [])
         self._phase_tags = phase_tags
-        self.packed = packed
+        self._packed = packed
+        self._packed_src = None  # a batch.SequenceBatch holding it on the device
+        self._breakdown = None
         self._arrays = arrays
+
+    @property
+    def packed(self):
+        """The packed pm_req_t replay records (host)."""
+        if self._packed is None and self._packed_src is not None:
+            self._packed = self._packed_src.packed(0)
+            self._packed_src = None
+        return self._packed
+
+    @packed.setter
+    def packed(self, value):
+        self._packed = value
+        self._packed_src = None
 
     def __len__(self) -> int:
         if self._requests is not None:
@@ -101,6 +116,8 @@ class RequestSequence:
 
     def breakdown(self) -> dict[str, int]:
         """Sum of ALLOC sizes per role value (estimator.py:160-164)."""
+        if self._breakdown is not None:
+            return dict(self._breakdown)
         if self._arrays is None:
             out: dict[str, int] = {}
             for r in self.requests:
@@ -185,7 +202,7 @@ class AnalyzedTrace:
     def _apply_final(self):
         """build_sequence mutates the analyzed blocks in place, like the
         reference (orchestration.py:222-223, 197)."""
-        roles, frees = self._final
+        roles, frees = self._final if isinstance(self._final, tuple) else self._final.get()
         for blk, rc, fr in zip(self._objects[2], roles.tolist(), frees.tolist()):
             blk.role = ROLE_OF_CODE[rc]
             blk.free_time = None if fr == NONE else fr
@@ -334,25 +351,71 @@ def build_sequence(analyzed: AnalyzedTrace, iterations: int = 2,
                            arrays=arrays)
 
 
+class _DeviceArrays(dict):
+    """RequestSequence arrays left on the device by pm_pipeline_batch's
+    views: read back on the first access of a column (the estimator needs
+    none of them)."""
+
+    def __init__(self, host: dict, dev: dict, n: int):
+        super().__init__(host)
+        self._dev = dev
+        self._n = n
+
+    def __missing__(self, key):
+        if key not in self._dev:
+            raise KeyError(key)
+        val = self._dev[key][:self._n].cpu().numpy()
+        self[key] = val
+        return val
+
+
+class _LazyFinal:
+    """analyzed._final of the batched path: (roles, frees), read back only
+    if the analyzed trace's block views are materialised."""
+
+    def __init__(self, dev: dict, nb: int):
+        self._dev, self._nb = dev, nb
+        self._val = None
+
+    def get(self):
+        if self._val is None:
+            self._val = (self._dev["fb_role"][:self._nb].cpu().numpy(),
+                         self._dev["fb_free"][:self._nb].cpu().numpy())
+        return self._val
+
+
+def _native_req_bytes() -> int:
+    from ._native import REQ_DTYPE
+    return REQ_DTYPE.itemsize
+
+
 def _build_batched(analyzed: AnalyzedTrace, plan, iterations: int) -> RequestSequence:
     """build_sequence through pm_pipeline_batch (B = 1) with its views:
-    link, orchestration and the total order on the device in one call."""
+    link, orchestration and the total order on the device in one call; the
+    views stay on the device until something reads them."""
     from .batch import build_sequences
     sb = build_sequences([analyzed.bundle], iterations, views=True)
     if sb.errors[0] is not None:
         raise sb.errors[0]
-    v = sb.views
     n = int(sb.req_off[1])
-    nb = int(v["blk_off"][1])
-    analyzed._final = (v["fb_role"][:nb].copy(), v["fb_free"][:nb].copy())
+    nb = int(sb.views["blk_off"][1])
+    # keep right-sized device copies only (the call's buffers are sized for
+    # the worst case)
+    v = {f: (t[:nb] if f.startswith("fb_") else t[:n]).clone()
+         for f, t in sb.views.items() if f != "blk_off"}
+    rs = _native_req_bytes()
+    sb.d_reqs = sb.d_reqs[:n * rs].clone()
+    sb.views = None
+    analyzed._final = _LazyFinal(v, nb)
     if analyzed._objects is not None:
         analyzed._apply_final()
-    arrays = {"n": n, "n_model": int(sb.n_model[0]),
-              **{f: v[f][:n].copy() for f in ("kind", "size", "vts", "tag", "a", "b",
-                                                "role", "raw")},
-              "batch_ids": plan.batch_ids}
-    return RequestSequence(iteration_boundaries=plan.boundaries, packed=sb.packed(0),
-                           arrays=arrays)
+    arrays = _DeviceArrays({"n": n, "n_model": int(sb.n_model[0]),
+                            "batch_ids": plan.batch_ids}, v, n)
+    seq = RequestSequence(iteration_boundaries=plan.boundaries, packed=None,
+                          arrays=arrays)
+    seq._packed_src = sb
+    seq._breakdown = sb.breakdown(0)
+    return seq
 
 
 __all__ = ["AnalyzedTrace", "MemoryRequest", "RequestKind", "RequestSequence",
