@@ -613,6 +613,31 @@ def other_configs(dev) -> dict:
                  "parity": "tests/test_c4_sweep.py, tests/test_config_goldens.py "
                            "(the reference's goldens on the grid)",
                  "timing": "CUDA events, best of 3"}
+    # C1 (and one C2 batch size): a captured trace file -> report, end to end
+    import gzip
+    import tempfile
+    import paper_2504_03887_b200 as eng
+    gold = json.loads((REPO / "tests" / "golden" / "captures_golden.json").read_text())
+    tdir = Path(tempfile.mkdtemp())
+    for key, name in (("c1", "resnet18_bs32_224"), ("c2_file_bs8", "gpt2_bs8_s128")):
+        src = REPO / "tests" / "golden" / "traces"
+        path = tdir / f"{name}.json"
+        path.write_bytes(gzip.open(src / f"{name}.trace.json.gz").read())
+        side = src / f"{name}.sidecar.json"
+        est = eng.PeakMemoryEstimator()
+        est.estimate(eng.parse_trace(path, sidecar=eng.load_sidecar(side)))  # warm
+        times, rep = [], None
+        for _ in range(5):
+            t0 = time.perf_counter()
+            rep = est.estimate(eng.parse_trace(path, sidecar=eng.load_sidecar(side)))
+            times.append(time.perf_counter() - t0)
+        out[key] = {"workload": f"{name}: trace file -> parse_trace -> "
+                                "PeakMemoryEstimator.estimate -> report",
+                    "file_mb": round(path.stat().st_size / 1e6, 1),
+                    "ms": 1e3 * statistics.median(times),
+                    "report_identical_to_reference": rep.canonical_json() ==
+                    gold[name]["report_default"],
+                    "timing": "wall clock, median of 5, warm"}
     # C5
     bundle = synth_events.generate(357200, 2)
     build_sequences([bundle], 2)  # warm (pool growth at this size)
