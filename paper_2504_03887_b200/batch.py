@@ -21,7 +21,6 @@ over `estimate` would.
 
 from __future__ import annotations
 
-import ctypes
 from dataclasses import dataclass
 
 import numpy as np
@@ -39,8 +38,7 @@ from .trace import NONE, EventCategory, TraceBundle
 class _Trace:
     cols: dict
     plan: object = None
-    error: BaseException | None = None  # first host-side failure
-    error_stage: int = 9                # 1 markers, 2 plan
+    error: BaseException | None = None  # the first host-side failure
 
 
 def _is_layer_column(bundle: TraceBundle, idx: np.ndarray) -> np.ndarray:
@@ -78,12 +76,12 @@ def _trace(bundle: TraceBundle, iterations: int) -> _Trace:
     try:
         markers = extract_markers(bundle.by_category(EventCategory.USER_ANNOTATION))
     except NoIterationMarkers as e:
-        tr.error, tr.error_stage = e, 1
+        tr.error = e
         return tr
     try:
         tr.plan = plan_sequence(markers, bundle.metadata, iterations)
     except (NoIterations, MissingBatchBytes) as e:
-        tr.error, tr.error_stage = e, 2
+        tr.error = e
     return tr
 
 
@@ -121,15 +119,25 @@ class SequenceBatch:
         return self.d_reqs[a * rs:b * rs].cpu().numpy().view(_native.REQ_DTYPE).copy()
 
 
-def build_sequences(bundles, iterations: int = 2, device: int = 0,
+def build_sequences(bundles, iterations: int = 2, device: int | None = None,
                     views: bool = False) -> SequenceBatch:
     """orchestration.build_sequence(orchestration.analyze(b), iterations) for
-    every bundle, in one pm_pipeline_batch call.  With views, the ordered
-    request columns and the blocks' final roles / frees come back too
-    (`SequenceBatch.views`)."""
+    every bundle, in one pm_pipeline_batch call on `device` (default: the
+    current CUDA device) and its current stream.  With views, the ordered
+    request columns and the blocks' final roles / frees come back too, left
+    on the device (`SequenceBatch.views`)."""
     import torch
 
     _native.require_device()
+    if device is None:
+        device = torch.cuda.current_device()
+    with torch.cuda.device(device):
+        return _build_sequences(bundles, iterations, device, views)
+
+
+def _build_sequences(bundles, iterations, device, views) -> SequenceBatch:
+    import torch
+
     bundles = list(bundles)
     B = len(bundles)
     if B == 0:
