@@ -74,7 +74,11 @@ class _FakeSeqs:
         import numpy as np
         self.errors = errors
         self.req_off = np.zeros(len(errors) + 1, np.int64)
-        self.d_reqs = None
+
+        class _Dev:  # stands in for a device tensor: only .device.index is read
+            class device:
+                index = 0
+        self.d_reqs = _Dev()
 
     def breakdown(self, t):
         return {}
@@ -88,7 +92,7 @@ def _fake_device_batch(calls):
     from paper_2504_03887_b200._native import RESULT_DTYPE
 
     class DB:
-        def __init__(self, reqs, offs, cfgs, cfg_of):
+        def __init__(self, reqs, offs, cfgs, cfg_of, device=0):
             self.n = len(offs) - 1
 
         def launch(self):
