@@ -83,6 +83,10 @@ def parse_args(argv=None):
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--cpu-sample-stride", type=int, default=10)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--shared-device", action="store_true",
+                    help="plumbing check on a one-GPU machine: every rank uses "
+                         "cuda:0 and the gloo backend (timings are not a "
+                         "scaling measurement)")
     ap.add_argument("--no-other-configs", action="store_true",
                     help="skip the C2 / C4 / C5 measurements beside the C3 line")
     ap.add_argument("--ref-check-traces", type=int, default=16)
@@ -294,6 +298,8 @@ def main():
     world = max(world, 1)
     rank = int(os.environ.get("RANK", 0))
     local = int(os.environ.get("LOCAL_RANK", 0))
+    if args.shared_device:
+        local = 0
     if args.impl == "reference":
         return run_reference(args, rank, world)
     if args.dry_run:
@@ -304,7 +310,10 @@ def main():
     if world > 1:
         import torch.distributed as dist
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.shared_device:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     if rank == 0:  # no-op when the in-tree libraries are up to date
         import __graft_entry__
         __graft_entry__.build()
@@ -367,10 +376,12 @@ def main():
         dist.barrier()
     elapsed_ms = t_all0.elapsed_time(t_all1)
     launch_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    # reductions live where the backend can reduce them (gloo: host)
+    rdev = torch.device("cpu") if args.shared_device else dev
     if dist:
-        t = torch.tensor([elapsed_ms], dtype=torch.float64, device=dev)
+        t = torch.tensor([elapsed_ms], dtype=torch.float64, device=rdev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ev = torch.tensor([float(events_per_step)], dtype=torch.float64, device=dev)
+        ev = torch.tensor([float(events_per_step)], dtype=torch.float64, device=rdev)
         dist.all_reduce(ev, op=dist.ReduceOp.SUM)
         max_ms, all_events = float(t.item()), float(ev.item())
     else:
@@ -394,7 +405,7 @@ def main():
         for _ in range(e2e_steps):
             out = fn()
         dt = time.perf_counter() - t0
-        tt = torch.tensor([dt], dtype=torch.float64, device=dev)
+        tt = torch.tensor([dt], dtype=torch.float64, device=rdev)
         if dist:
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         return out, all_events * e2e_steps / float(tt.item())
@@ -536,6 +547,9 @@ def main():
                       "frac": value / (ceiling * world),
                       "source": "profiles/replay_ncu_summary.json (ncu --set full "
                                 "of the replay kernel: instructions, DRAM bytes)"})
+    if args.shared_device:
+        line["shared_device"] = ("plumbing check: every rank on cuda:0 over gloo; "
+                                 "not a scaling measurement")
     if world == 1 and not args.no_other_configs:
         line["other_configs"] = other_configs(dev)
     print(json.dumps(line))
