@@ -48,6 +48,7 @@ from .analysis import (
     extract_markers,
     group_memory_events,
 )
+from .batch import SequenceBatch, build_sequences
 from .estimator import EstimateReport, PeakMemoryEstimator
 from .linking import LayerMemoryProfile, link
 from .metrics import (
