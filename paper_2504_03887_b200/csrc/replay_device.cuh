@@ -1170,7 +1170,9 @@ struct Ctl {
   unsigned work[8];   // work counters: main pass, tiers 1..4
   unsigned n_list[8]; // traces queued for tier k (index 1..4)
   unsigned long long ck_used;  // checkpoint region bump counter (narrow passes)
-  unsigned pad[46];
+  unsigned main_exited;        // main-pass CTAs finished
+  unsigned main_done;          // 1 once every main-pass CTA has finished
+  unsigned pad[44];
 };
 
 // Shared-memory layout of the main kernel (per CTA): the bucket pool

@@ -1777,7 +1777,17 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
     if (lane == 0) atomicSub(active, 1);
     const int sts = results[tr].status;
     if (sts == PM_POOL_OVERFLOW) dir.release_victim_token();
-    if (lane == 0) route(ctl, sts, tr, kTierMemSmem, overflow_list, enc_list);
+    if (lane == 0) {
+      __threadfence();  // the trace's records / checkpoint before its list entry
+      route(ctl, sts, tr, kTierMemSmem, overflow_list, enc_list);
+    }
+  }
+  // a pass-1 grid running beside the main pass learns here that no more
+  // traces will be handed over (every list entry precedes the flag)
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(&ctl->main_exited, 1u) + 1u == gridDim.x) atomicExch(&ctl->main_done, 1u);
   }
 }
 
@@ -1801,7 +1811,8 @@ __global__ void __launch_bounds__(256, 1)
                              const u64* __restrict__ wire,
                              pm_req_t* __restrict__ expand, int long_trace,
                              long long* __restrict__ ck_off, char* __restrict__ ck_base,
-                             unsigned long long ck_cap, size_t warp_bytes) {
+                             unsigned long long ck_cap, size_t warp_bytes,
+                             int beside_main) {
   extern __shared__ __align__(16) char smem[];
   const int lane = threadIdx.x & 31;
   // each warp of the CTA owns a slice of the shared memory (its staging,
@@ -1836,13 +1847,44 @@ __global__ void __launch_bounds__(256, 1)
     mbar_fence_init();
   }
   __syncwarp();
-  const unsigned n = ctl->n_list[pass];
+  const unsigned n = beside_main ? 0u : ctl->n_list[pass];
   for (;;) {
     unsigned t = 0;
     if (lane == 0) t = atomicAdd(&ctl->work[pass], 1u);
     t = __shfl_sync(kFull, t, 0);
-    if (t >= n) break;
-    const int tr = list[t];
+    int tr;
+    if (!beside_main) {
+      if (t >= n) break;
+      tr = list[t];
+    } else {
+      // running beside the main pass (batches of one wave): wait until the
+      // main pass has handed over entry t -- or has finished without it
+      // (list slots start at -1; an entry is published after its data)
+      tr = -1;
+      if (lane == 0) {
+        for (;;) {
+          const unsigned cnt = *(volatile unsigned*)&ctl->n_list[pass];
+          if (t < cnt) {
+            const int v = *(volatile const int*)&list[t];
+            if (v >= 0) {
+              tr = v;
+              break;
+            }
+          } else if (*(volatile unsigned*)&ctl->main_done) {
+            if (t >= *(volatile unsigned*)&ctl->n_list[pass]) {
+              tr = -2;
+              break;
+            }
+            continue;
+          }
+          __nanosleep(4000);
+        }
+        __threadfence();  // acquire: the entry's records / checkpoint
+      }
+      tr = __shfl_sync(kFull, tr, 0);
+      __syncwarp();
+      if (tr == -2) break;
+    }
     // the last narrow tier expands wire words for the wide tier it hands to
     replay_trace(tr, reqs, offs, cfgs, cfg_of, results, timeline, recs, P, dir,
                  sg, lane, wire, expand, !SMEM_POOL,
