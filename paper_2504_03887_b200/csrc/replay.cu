@@ -392,35 +392,21 @@ int replay_batch_impl(const pm_req_t* reqs, const int64_t* trace_offsets,
   // pass (one trace per SM or fewer): otherwise they share the main pass's
   // throughput like any other trace
   const int long_trace = n_traces <= occ.sms ? pmn::kLongTrace : pmn::kNoSkip;
-  // A batch of about one wave (every trace starts at once; C4-like sweeps)
-  // is as slow as its slowest replay, and a replay that outgrows the main
-  // pass would otherwise continue only after the whole main pass: keep R
-  // SMs for a narrow pass 1 that runs BESIDE the main pass and picks the
-  // hand-offs up as they come (PM_BESIDE=0 disables).
-  int beside_sms = 0;
+  // Narrow pass 1 runs BESIDE the main pass: launched right behind it as a
+  // programmatic dependent launch (the main pass's CTAs release it once they
+  // are all resident, so it can never take SMs the main pass needs), its
+  // CTAs take SMs the main pass leaves idle (a batch of less than a wave)
+  // or frees as its CTAs finish, and continue hand-offs as they arrive
+  // instead of after the whole main pass -- a replay that outgrows the main
+  // pass early (C4's fragmenting configs) no longer waits for the slowest
+  // main replay (PM_BESIDE=0: pass 1 after the main pass).
+  bool beside = false;
   {
     const char* env = getenv("PM_BESIDE");
-    const long long slots = (long long)occ.per_sm_n * occ.sms * mwarps;
-    if (narrow && ready == nullptr && n_traces > occ.sms && n_traces <= slots &&
-        !(env && atoi(env) == 0) && occ.sms >= 32 && occ.per_sm_n == 1) {
-      beside_sms = occ.sms / 6;
-      if (grid > occ.sms - beside_sms) grid = occ.sms - beside_sms;
-    }
+    beside = narrow && ready == nullptr && !(env && atoi(env) == 0);
   }
-  static cudaStream_t side = nullptr;  // the beside pass's stream (per process)
-  cudaEvent_t ev_start = nullptr, ev_side = nullptr;
-  if (beside_sms > 0) {
-    static std::mutex mu;
-    std::lock_guard<std::mutex> g(mu);
-    if (!side) {
-      e = cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking);
-      if (e != cudaSuccess) return cuda_fail(e, "cudaStreamCreate (beside)");
-    }
+  if (beside) {
     e = cudaMemsetAsync(list_m1, 0xFF, 4 * nt, stream);  // slots start at -1
-    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_start, cudaEventDisableTiming);
-    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_side, cudaEventDisableTiming);
-    if (e == cudaSuccess) e = cudaEventRecord(ev_start, stream);
-    if (e == cudaSuccess) e = cudaStreamWaitEvent(side, ev_start, 0);
     if (e != cudaSuccess) return cuda_fail(e, "beside pass setup");
   }
 #define PM_LAUNCH_NARROW(W)                                                   \
@@ -461,16 +447,23 @@ int replay_batch_impl(const pm_req_t* reqs, const int64_t* trace_offsets,
     if (rc2 != PM_SUCCESS) return rc2;
   }
   const long long gtraces = n_traces < occ.sms ? n_traces : occ.sms;
-  if (beside_sms > 0) {
-    pmn::replay_narrow_mem_kernel<true>
-        <<<(unsigned)beside_sms, 32 * occ.warps_s1, occ.warps_s1 * occ.warp_bytes_s1, side>>>(
-            reqs, trace_offsets, cfgs, cfg_of_trace, results, timeline,
-            reinterpret_cast<pmb::u32*>(recs), ctl, pmn::kTierMemSmem, list_m1, list_mb,
-            list_w1, nullptr, occ.nbmax_s1, reinterpret_cast<const pmb::u64*>(wire),
-            const_cast<pm_req_t*>(reqs), long_trace, ck_off, ck_base, ck_cap,
-            occ.warp_bytes_s1, 1);
-    e = cudaGetLastError();
-    if (e == cudaSuccess) e = cudaEventRecord(ev_side, side);
+  if (beside) {
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3((unsigned)gtraces);
+    lc.blockDim = dim3(32 * occ.warps_s1);
+    lc.dynamicSmemBytes = (size_t)occ.warps_s1 * occ.warp_bytes_s1;
+    lc.stream = stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    e = cudaLaunchKernelEx(&lc, pmn::replay_narrow_mem_kernel<true>, reqs, trace_offsets, cfgs,
+                           cfg_of_trace, results, timeline, reinterpret_cast<pmb::u32*>(recs),
+                           ctl, (int)pmn::kTierMemSmem, (const int32_t*)list_m1, list_mb,
+                           list_w1, (char*)nullptr, occ.nbmax_s1,
+                           reinterpret_cast<const pmb::u64*>(wire), const_cast<pm_req_t*>(reqs),
+                           long_trace, ck_off, ck_base, ck_cap, (size_t)occ.warp_bytes_s1, 1);
     if (e != cudaSuccess) return cuda_fail(e, "replay beside-pass launch");
   }
   // passes 1-2: narrow, shared-memory directory (entries in shared memory,
@@ -478,21 +471,16 @@ int replay_batch_impl(const pm_req_t* reqs, const int64_t* trace_offsets,
   // pass 1: several warps per SM, each with a private shared-memory pool
   // (fragmented traces replay side by side); pass 2: one warp owning the
   // SM's shared memory for the traces that outgrow those
-  pmn::replay_narrow_mem_kernel<true>
-      <<<(unsigned)gtraces, 32 * occ.warps_s1, occ.warps_s1 * occ.warp_bytes_s1, stream>>>(
-          reqs, trace_offsets, cfgs, cfg_of_trace, results, timeline,
-          reinterpret_cast<pmb::u32*>(recs), ctl, pmn::kTierMemSmem, list_m1, list_mb,
-          list_w1, nullptr, occ.nbmax_s1, reinterpret_cast<const pmb::u64*>(wire),
-          const_cast<pm_req_t*>(reqs), long_trace, ck_off, ck_base, ck_cap,
-          occ.warp_bytes_s1, 0);
-  e = cudaGetLastError();
-  if (e != cudaSuccess) return cuda_fail(e, "replay pass-1 launch");
-  if (beside_sms > 0) {
-    // pass 1 is complete when both of its grids are: join before pass 1b
-    e = cudaStreamWaitEvent(stream, ev_side, 0);
-    cudaEventDestroy(ev_start);
-    cudaEventDestroy(ev_side);
-    if (e != cudaSuccess) return cuda_fail(e, "beside pass join");
+  if (!beside) {
+    pmn::replay_narrow_mem_kernel<true>
+        <<<(unsigned)gtraces, 32 * occ.warps_s1, occ.warps_s1 * occ.warp_bytes_s1, stream>>>(
+            reqs, trace_offsets, cfgs, cfg_of_trace, results, timeline,
+            reinterpret_cast<pmb::u32*>(recs), ctl, pmn::kTierMemSmem, list_m1, list_mb,
+            list_w1, nullptr, occ.nbmax_s1, reinterpret_cast<const pmb::u64*>(wire),
+            const_cast<pm_req_t*>(reqs), long_trace, ck_off, ck_base, ck_cap,
+            occ.warp_bytes_s1, 0);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "replay pass-1 launch");
   }
   pmn::replay_narrow_mem_kernel<true><<<(unsigned)gtraces, 32, occ.smem_m1, stream>>>(
       reqs, trace_offsets, cfgs, cfg_of_trace, results, timeline,

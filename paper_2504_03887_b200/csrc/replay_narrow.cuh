@@ -1727,6 +1727,9 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
                          long long* __restrict__ ck_off, char* __restrict__ ck_base,
                          unsigned long long ck_cap) {
   extern __shared__ __align__(16) char smem[];
+  // every CTA of this grid is resident: the pass-1 grid launched behind it
+  // (a programmatic dependent launch) may start on the SMs it leaves free
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
   NCk ck;
