@@ -382,8 +382,18 @@ int replay_batch_impl(const pm_req_t* reqs, const int64_t* trace_offsets,
   const bool narrow = occ.narrow || wire != nullptr;  // wire words need it
   const int mwarps = narrow && !occ.narrow ? kNarrowWarps : occ.warps;
   long long want = ((long long)n_traces + mwarps - 1) / mwarps;
-  long long grid = (long long)(narrow && !occ.narrow ? occ.per_sm_n : occ.per_sm) * occ.sms;
+  const long long full = (long long)(narrow && !occ.narrow ? occ.per_sm_n : occ.per_sm) * occ.sms;
+  long long grid = full;
   if (want < grid) grid = want;
+  // Under half a wave (a small sweep, a rank's shard at 8 GPUs): spread the
+  // traces over every SM rather than packing them into the fewest CTAs --
+  // a warp's chain is shorter when fewer warps share its SM
+  const char* spread_env = getenv("PM_SPREAD");
+  if (narrow && 2 * (long long)n_traces <= full * mwarps &&
+      !(spread_env && atoi(spread_env) == 0)) {
+    const long long spread = n_traces < occ.sms ? n_traces : occ.sms;
+    if (spread > grid) grid = spread < full ? spread : full;
+  }
   if (const char* cap = getenv("PM_MAX_GRID")) {  // debugging aid
     const long long g = atoll(cap);
     if (g > 0 && g < grid) grid = g;
