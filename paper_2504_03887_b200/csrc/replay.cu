@@ -402,15 +402,6 @@ int replay_batch_impl(const pm_req_t* reqs, const int64_t* trace_offsets,
   // pass (one trace per SM or fewer): otherwise they share the main pass's
   // throughput like any other trace
   const int long_trace = n_traces <= occ.sms ? pmn::kLongTrace : pmn::kNoSkip;
-  // ... except pass 1b (one warp owning the SM's shared memory): a long
-  // trace replays there with its entries in shared memory until it
-  // outgrows them, then continues in pass 2 from its checkpoint
-  // (PM_LONG_1B=0: straight to pass 2)
-  int long_skip_1b = long_trace;
-  {
-    const char* env = getenv("PM_LONG_1B");
-    if (!(env && atoi(env) == 0)) long_skip_1b = pmn::kNoSkip;
-  }
   // Narrow pass 1 runs BESIDE the main pass: launched right behind it as a
   // programmatic dependent launch (the main pass's CTAs release it once they
   // are all resident, so it can never take SMs the main pass needs), its
@@ -505,7 +496,7 @@ int replay_batch_impl(const pm_req_t* reqs, const int64_t* trace_offsets,
       reqs, trace_offsets, cfgs, cfg_of_trace, results, timeline,
       reinterpret_cast<pmb::u32*>(recs), ctl, pmn::kTierMemSmemBig, list_mb, list_m2,
       list_w1, nullptr, occ.nbmax_m1, reinterpret_cast<const pmb::u64*>(wire),
-      const_cast<pm_req_t*>(reqs), long_skip_1b, ck_off, ck_base, ck_cap, 0, 0);
+      const_cast<pm_req_t*>(reqs), long_trace, ck_off, ck_base, ck_cap, 0, 0);
   e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "replay pass-2 launch");
   {
