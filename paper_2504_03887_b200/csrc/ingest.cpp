@@ -28,9 +28,13 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <string_view>
 #include <thread>
-#include <unordered_map>
 #include <vector>
+
+#if defined(__SSE2__)
+#include <emmintrin.h>
+#endif
 
 #include <openssl/evp.h>
 
@@ -50,7 +54,11 @@ struct Cols {
   std::vector<int8_t> cat;
   std::vector<int64_t> ints[F_N];
   std::vector<int32_t> name_id;    // per event, into the table below
-  std::unordered_map<std::string, int32_t> intern;
+  // open-addressing set of the distinct names: slot -> name id + 1 (0 =
+  // empty), keyed by the name's bytes in `names`; hash beside it
+  std::vector<int32_t> slot;
+  std::vector<uint64_t> slot_hash;
+  int32_t n_names = 0;
   std::string names;               // distinct names, UTF-8
   std::vector<int64_t> name_off;   // code-point offsets, n_names+1
   std::vector<int64_t> name_boff;  // byte offsets into `names`, n_names+1
@@ -82,6 +90,61 @@ struct Parser {
 
   void ws() {
     while (p < end && (*p == ' ' || *p == '\n' || *p == '\r' || *p == '\t')) ++p;
+  }
+  // first byte at or after q that is '"', '\\' or a control character
+  // (< 0x20), or end: 16 bytes per step where the buffer allows
+  const char* run_end(const char* q) const {
+#if defined(__SSE2__)
+    const __m128i quote = _mm_set1_epi8('"'), bslash = _mm_set1_epi8('\\'),
+                  ctl = _mm_set1_epi8(0x1F);
+    while (end - q >= 16) {
+      const __m128i x = _mm_loadu_si128(reinterpret_cast<const __m128i*>(q));
+      const __m128i hit = _mm_or_si128(
+          _mm_or_si128(_mm_cmpeq_epi8(x, quote), _mm_cmpeq_epi8(x, bslash)),
+          _mm_cmpeq_epi8(_mm_max_epu8(x, ctl), ctl));
+      const int m = _mm_movemask_epi8(hit);
+      if (m) return q + __builtin_ctz((unsigned)m);
+      q += 16;
+    }
+#endif
+    while (q < end && *q != '"' && *q != '\\' && (unsigned char)*q >= 0x20) ++q;
+    return q;
+  }
+  // skip a string (p at its opening quote) with the same checks as str():
+  // control characters, escapes and surrogate pairs
+  void skip_str() {
+    ++p;
+    while (true) {
+      p = run_end(p);
+      if (p >= end) throw Unsupported();
+      const char c = *p;
+      if (c == '"') {
+        ++p;
+        return;
+      }
+      if (c != '\\') throw Unsupported();  // control character
+      ++p;
+      if (p >= end) throw Unsupported();
+      const char e = *p++;
+      switch (e) {
+        case '"': case '\\': case '/': case 'b': case 'f': case 'n': case 'r':
+        case 't':
+          break;
+        case 'u': {
+          const uint32_t cp = hex4();
+          if (cp >= 0xD800 && cp < 0xDC00) {
+            if (end - p < 6 || p[0] != '\\' || p[1] != 'u') throw Unsupported();
+            p += 2;
+            const uint32_t lo = hex4();
+            if (lo < 0xDC00 || lo >= 0xE000) throw Unsupported();
+          } else if (cp >= 0xDC00 && cp < 0xE000) {
+            throw Unsupported();
+          }
+          break;
+        }
+        default: throw Unsupported();
+      }
+    }
   }
   char peek() {
     ws();
@@ -128,6 +191,7 @@ struct Parser {
     std::string out;
     const char* run = p;
     while (true) {
+      p = run_end(p);
       if (p >= end) throw Unsupported();
       const unsigned char c = (unsigned char)*p;
       if (c == '"') {
@@ -136,10 +200,6 @@ struct Parser {
         return out;
       }
       if (c < 0x20) throw Unsupported();
-      if (c != '\\') {
-        ++p;
-        continue;
-      }
       out.append(run, p - run);
       ++p;
       if (p >= end) throw Unsupported();
@@ -174,17 +234,17 @@ struct Parser {
   }
   // object key without copying when it has no escapes; escaped keys decode
   // into `scratch`
-  std::pair<const char*, size_t> key(std::string& scratch) {
+  std::string_view key(std::string& scratch) {
     expect('"');
     const char* s = p;
-    while (p < end && *p != '"' && *p != '\\' && (unsigned char)*p >= 0x20) ++p;
+    p = run_end(p);
     if (p < end && *p == '"') {
       ++p;
       return {s, (size_t)(p - 1 - s)};
     }
     p = s - 1;
     scratch = str();
-    return {scratch.data(), scratch.size()};
+    return scratch;
   }
   // number token: kind 1 = integer, 2 = float
   int number(const char** s, const char** e) {
@@ -222,9 +282,9 @@ struct Parser {
     if (c == '{') {
       ++p;
       if (peek() == '}') { ++p; return; }
-      std::string scratch;
       while (true) {
-        key(scratch);
+        if (peek() != '"') throw Unsupported();
+        skip_str();
         expect(':');
         skip();
         const char d = peek();
@@ -243,7 +303,7 @@ struct Parser {
         if (d != ',') throw Unsupported();
       }
     } else if (c == '"') {
-      str();
+      skip_str();
     } else if (c == 't') {
       literal("true");
     } else if (c == 'f') {
@@ -258,19 +318,21 @@ struct Parser {
 };
 
 // A scalar JSON value as the reference sees it after json.loads.
+// Strings are views into the text unless they hold escapes (then decoded
+// into `own`); a Val is filled in place and not copied.
 struct Val {
   enum T { ABSENT, NUL, INT, FLT, STR, TRUE_, FALSE_, OTHER } t = ABSENT;
   int64_t i = 0;
   double f = 0;
-  std::string s;
+  std::string_view s;
+  std::string own;
 };
 
-Val scalar(Parser& P) {
-  Val v;
+void scalar(Parser& P, Val& v) {
   const char c = P.peek();
   if (c == '"') {
     v.t = Val::STR;
-    v.s = P.str();
+    v.s = P.key(v.own);
   } else if (c == 'n') {
     P.literal("null");
     v.t = Val::NUL;
@@ -307,7 +369,6 @@ Val scalar(Parser& P) {
         throw Unsupported();
     }
   }
-  return v;
 }
 
 // _as_int (trace.py:140-146): None -> None, int(value) otherwise
@@ -339,24 +400,48 @@ bool truthy(const Val& v) {  // `x or 0`
   }
 }
 
-int32_t intern_name(Cols& C, const std::string& s) {
-  auto it = C.intern.find(s);
-  if (it != C.intern.end()) return it->second;
-  const int32_t id = (int32_t)C.intern.size();
-  C.intern.emplace(s, id);
+int32_t intern_name(Cols& C, std::string_view s) {
+  const uint64_t h = std::hash<std::string_view>{}(s);
+  if (2 * ((size_t)C.n_names + 1) > C.slot.size()) {
+    // grow: re-place every name by its stored hash
+    const size_t cap = std::max<size_t>(64, 2 * C.slot.size());
+    std::vector<int32_t> slot(cap, 0);
+    std::vector<uint64_t> sh(cap, 0);
+    for (size_t k = 0; k < C.slot.size(); ++k) {
+      if (C.slot[k] == 0) continue;
+      size_t q = C.slot_hash[k] & (cap - 1);
+      while (slot[q] != 0) q = (q + 1) & (cap - 1);
+      slot[q] = C.slot[k];
+      sh[q] = C.slot_hash[k];
+    }
+    C.slot.swap(slot);
+    C.slot_hash.swap(sh);
+  }
+  const size_t mask = C.slot.size() - 1;
+  size_t k = h & mask;
+  for (; C.slot[k] != 0; k = (k + 1) & mask) {
+    if (C.slot_hash[k] != h) continue;
+    const int32_t id = C.slot[k] - 1;
+    const int64_t b = C.name_boff[id], e = C.name_boff[id + 1];
+    if ((size_t)(e - b) == s.size() && memcmp(C.names.data() + b, s.data(), s.size()) == 0)
+      return id;
+  }
+  const int32_t id = C.n_names++;
+  C.slot[k] = id + 1;
+  C.slot_hash[k] = h;
   int64_t n = 0;
   for (unsigned char c : s)
     if ((c & 0xC0) != 0x80) ++n;
   C.cp_total += n;
-  C.names += s;
+  C.names.append(s.data(), s.size());
   C.name_off.push_back(C.cp_total);
   C.name_boff.push_back((int64_t)C.names.size());
   return id;
 }
 
 template <size_t N>
-inline bool is(const std::pair<const char*, size_t>& k, const char (&w)[N]) {
-  return k.second == N - 1 && memcmp(k.first, w, N - 1) == 0;
+inline bool is(std::string_view k, const char (&w)[N]) {
+  return k.size() == N - 1 && memcmp(k.data(), w, N - 1) == 0;
 }
 
 // one record object; appends a row or drops it
@@ -374,13 +459,13 @@ void record(Parser& P, Cols& C, bool strict) {
     while (true) {
       const auto key = P.key(scratch);
       P.expect(':');
-      if (is(key, "ph")) ph = scalar(P);
-      else if (is(key, "cat")) cat = scalar(P);
-      else if (is(key, "name")) name = scalar(P);
-      else if (is(key, "ts")) ts = scalar(P);
-      else if (is(key, "dur")) dur = scalar(P);
+      if (is(key, "ph")) scalar(P, ph);
+      else if (is(key, "cat")) scalar(P, cat);
+      else if (is(key, "name")) scalar(P, name);
+      else if (is(key, "ts")) scalar(P, ts);
+      else if (is(key, "dur")) scalar(P, dur);
       else if (is(key, "args")) {
-        for (auto& x : a) x = Val();
+        for (auto& x : a) x.t = Val::ABSENT;
         args_other = false;
         has_args = true;
         if (P.peek() == '{') {
@@ -399,7 +484,7 @@ void record(Parser& P, Cols& C, bool strict) {
               else if (is(k, "Bytes")) f = F_BYTES;
               else if (is(k, "Total Allocated")) f = F_TA;
               else if (is(k, "Total Reserved")) f = F_TR;
-              if (f >= 0) a[f] = scalar(P);
+              if (f >= 0) scalar(P, a[f]);
               else P.skip();
               const char d = P.peek();
               ++P.p;
@@ -408,7 +493,8 @@ void record(Parser& P, Cols& C, bool strict) {
             }
           }
         } else {
-          const Val v = scalar(P);  // `args or {}`: falsy -> {}
+          Val v;  // `args or {}`: falsy -> {}
+          scalar(P, v);
           if (truthy(v) || v.t == Val::OTHER) args_other = true;
         }
       } else {
@@ -433,7 +519,7 @@ void record(Parser& P, Cols& C, bool strict) {
   } else if (strict) {
     throw Unsupported();
   }
-  std::string nm;
+  std::string_view nm;
   if (name.t == Val::STR) nm = name.s;
   else if (name.t != Val::ABSENT) throw Unsupported();  // str(non-string)
   if (ts.t != Val::INT && ts.t != Val::FLT) throw Unsupported();  // incl. missing
@@ -570,9 +656,18 @@ struct Out {
 
 // Strict UTF-8 validation (the reference reads the file with
 // encoding="utf-8"; invalid input goes to the Python reader, which raises the
-// reference's error).  ASCII runs are skipped 8 bytes at a time.
+// reference's error).  ASCII runs are skipped 32 bytes at a time (SSE2) or 8.
 bool valid_utf8(const unsigned char* p, const unsigned char* end) {
   while (p < end) {
+#if defined(__SSE2__)
+    // ASCII runs 32 bytes at a time
+    while (end - p >= 32) {
+      const __m128i a = _mm_loadu_si128(reinterpret_cast<const __m128i*>(p));
+      const __m128i b = _mm_loadu_si128(reinterpret_cast<const __m128i*>(p + 16));
+      if (_mm_movemask_epi8(_mm_or_si128(a, b)) != 0) break;
+      p += 32;
+    }
+#endif
     if (end - p >= 8) {
       uint64_t w;
       memcpy(&w, p, 8);
@@ -612,8 +707,9 @@ void adopt_part(Cols& A, Cols&& B) {
   const size_t nb = B.name_boff.size() - 1;
   std::vector<int32_t> map(nb);
   for (size_t k = 0; k < nb; ++k)
-    map[k] = intern_name(A, B.names.substr((size_t)B.name_boff[k],
-                                           (size_t)(B.name_boff[k + 1] - B.name_boff[k])));
+    map[k] = intern_name(A, std::string_view(B.names).substr(
+                                (size_t)B.name_boff[k],
+                                (size_t)(B.name_boff[k + 1] - B.name_boff[k])));
   A.dropped += B.dropped;
   A.parts.push_back(std::move(B));
   A.remap.push_back(std::move(map));
@@ -806,7 +902,7 @@ int pm_ingest_json(const char* text, int64_t len, int strict, void** handle) {
 
 int64_t pm_ingest_count(void* h) { return static_cast<Cols*>(h)->rows(); }
 int64_t pm_ingest_dropped(void* h) { return static_cast<Cols*>(h)->dropped; }
-int64_t pm_ingest_n_names(void* h) { return (int64_t)static_cast<Cols*>(h)->intern.size(); }
+int64_t pm_ingest_n_names(void* h) { return static_cast<Cols*>(h)->n_names; }
 int64_t pm_ingest_names_bytes(void* h) { return (int64_t)static_cast<Cols*>(h)->names.size(); }
 
 // Copy the columns out: ints is F_N x n (field-major: python id, parent id,

@@ -333,3 +333,19 @@ def test_invalid_utf8_declined_and_parse_trace_raises(tmp_path):
     f.write_bytes(good.replace(b"\\u00e9", b"\xc3"))
     with pytest.raises(MalformedTrace, match="not valid JSON"):
         parse_trace(f)
+
+
+@pytest.mark.parametrize("special", ['\\"', "\\\\", "\\n", "\\u00e9", "\\ud83d\\ude00",
+                                     "\x01", "\x1f", "\\x", "\\ud800", "é", "\x7f"])
+def test_string_scan_around_16_byte_steps(special):
+    """The string scanner steps 16 bytes at a time: an escape, a control
+    character or the closing quote at every offset of a step (in a name, in
+    a skipped value and in a key) reads like the Python reader or is
+    declined where the reference errors."""
+    for pos in range(0, 40):
+        body = "a" * pos + special + "b" * (pos % 7)
+        for rec in ('{"name": "%s", "ts": 1, "cat": "cpu_op"}' % body,
+                    '{"name": "n", "ts": 1, "cat": "cpu_op", "x": "%s"}' % body,
+                    '{"name": "n", "ts": 1, "cat": "cpu_op", "args": {"%s": 1}}' % body):
+            check_text('{"traceEvents": [%s]}' % rec)
+            check_text('[%s]' % rec)  # the closing quote near the end of the text
