@@ -74,6 +74,9 @@ def main():
     ap.add_argument("--caps", default=str(REPO / "data" / "captures"))
     ap.add_argument("--capture", action="store_true")
     ap.add_argument("--jobs", type=int, default=4)
+    ap.add_argument("--profile", action="store_true",
+                    help="cProfile of the batched parse + estimate_many to stderr")
+    ap.add_argument("--no-reference", action="store_true")
     args = ap.parse_args()
     caps = Path(args.caps)
     out = {"config": "C2: GPT-2 small (124M) training traces, batch 1..64 x seq 128, "
@@ -91,10 +94,13 @@ def main():
     # reference, one process per file
     ctx = mp.get_context("fork")
     procs = len(os.sched_getaffinity(0))
-    t0 = time.perf_counter()
-    with ctx.Pool(procs) as pool:
-        ref = pool.map(_ref_one, files, chunksize=1)
-    ref_wall = time.perf_counter() - t0
+    if args.no_reference:
+        ref, ref_wall = [(None, float("nan"))] * len(files), float("nan")
+    else:
+        t0 = time.perf_counter()
+        with ctx.Pool(procs) as pool:
+            ref = pool.map(_ref_one, files, chunksize=1)
+        ref_wall = time.perf_counter() - t0
     ref_reports = [r for r, _ in ref]
     out["reference"] = {"wall_s": ref_wall, "processes": procs,
                         "serial_s": sum(t for _, t in ref)}
@@ -131,6 +137,16 @@ def main():
     out["speedup_batched_vs_reference_wall"] = ref_wall / (t2 - t0)
     out["speedup_batched_vs_reference_serial"] = out["reference"]["serial_s"] / (t2 - t0)
     print(json.dumps(out), flush=True)
+    if args.profile:
+        import cProfile
+        import pstats
+        pr = cProfile.Profile()
+        pr.enable()
+        with ThreadPoolExecutor(max_workers=8) as pool:
+            bundles = list(pool.map(parse, files))
+        est.estimate_many(bundles)
+        pr.disable()
+        pstats.Stats(pr, stream=sys.stderr).sort_stats("cumtime").print_stats(40)
 
 
 if __name__ == "__main__":
