@@ -87,6 +87,13 @@ struct Occupancy {
   bool narrow = true;  // main pass: replay_narrow_kernel (else the wide kernel)
   int per_sm_n = 0, buckets_n = 0;  // the narrow main kernel's launch
   size_t smem_n = 0;
+  // batches under a wave: the narrowest main-kernel CTA that holds the
+  // batch with one trace per warp -- 1, 12, 16 or 20 warps per CTA
+  // (kSmallWidths): fewer warps share an SM's pool and issue slots, and they
+  // compile to 96 registers instead of 80 (PM_REPLAY_WARPS pins the width)
+  int per_sm_w[4] = {0, 0, 0, 0}, buckets_w[4] = {0, 0, 0, 0};
+  size_t smem_w[4] = {0, 0, 0, 0};
+  bool warps_pinned = false;
   int nbmax_m1 = 0, nbmax_m2 = 0;   // narrow memory-directory passes 2-3
   size_t smem_m1 = 0;
   int warps_s1 = 0, nbmax_s1 = 0;   // pass 1: warps per SM, buckets per warp
@@ -100,6 +107,7 @@ struct Occupancy {
 };
 
 constexpr int kTier1Warps = 8;  // tier 1: a dedicated 32-bucket pool per warp
+constexpr int kSmallWidths[4] = {1, 12, 16, 20};
 
 template <int W>
 int setup_kernel(int optin, int cap, int* buckets, size_t* smem, int* per_sm) {
@@ -162,8 +170,18 @@ int query_occupancy(Occupancy* out) {
     const char* wide = getenv("PM_REPLAY_WIDE");
     o.narrow = !(wide && atoi(wide) != 0);
     o.warps = o.narrow ? kNarrowWarps : kWarps;
-    if (const char* env = getenv("PM_REPLAY_WARPS")) o.warps = atoi(env);
-    int rc;
+    if (const char* env = getenv("PM_REPLAY_WARPS")) {
+      o.warps = atoi(env);
+      o.warps_pinned = true;
+    }
+    int rc = setup_narrow<1>(optin, cap, &o.buckets_w[0], &o.smem_w[0], &o.per_sm_w[0]);
+    if (rc == PM_SUCCESS)
+      rc = setup_narrow<12>(optin, cap, &o.buckets_w[1], &o.smem_w[1], &o.per_sm_w[1]);
+    if (rc == PM_SUCCESS)
+      rc = setup_narrow<16>(optin, cap, &o.buckets_w[2], &o.smem_w[2], &o.per_sm_w[2]);
+    if (rc == PM_SUCCESS)
+      rc = setup_narrow<20>(optin, cap, &o.buckets_w[3], &o.smem_w[3], &o.per_sm_w[3]);
+    if (rc != PM_SUCCESS) return rc;
     // the narrow main kernel is always set up (wire-word input needs it even
     // when PM_REPLAY_WIDE selects the wide main pass)
     const int nw = o.narrow ? o.warps : kNarrowWarps;
@@ -389,10 +407,28 @@ int replay_batch_impl(const pm_req_t* reqs, const int64_t* trace_offsets,
   // traces over every SM rather than packing them into the fewest CTAs --
   // a warp's chain is shorter when fewer warps share its SM
   const char* spread_env = getenv("PM_SPREAD");
-  if (narrow && 2 * (long long)n_traces <= full * mwarps &&
-      !(spread_env && atoi(spread_env) == 0)) {
+  int lwarps = mwarps;  // the narrow main kernel's width for this launch
+  size_t lsmem = occ.smem_n;
+  int lbuckets = occ.buckets_n;
+  const bool spread_ok = !(spread_env && atoi(spread_env) == 0);
+  if (narrow && 2 * (long long)n_traces <= full * mwarps && spread_ok) {
     const long long spread = n_traces < occ.sms ? n_traces : occ.sms;
     if (spread > grid) grid = spread < full ? spread : full;
+  }
+  // and in the narrowest CTAs that hold the batch (C3 traces: 148 traces one
+  // warp per CTA 80 vs 105 ms; 600-1776 traces 12 warps per CTA 15-19 %
+  // faster than 24)
+  if (narrow && spread_ok && !occ.warps_pinned) {
+    for (int k = 0; k < 4; ++k) {
+      const long long slots = (long long)kSmallWidths[k] * occ.sms * occ.per_sm_w[k];
+      if (n_traces > slots) continue;
+      lwarps = kSmallWidths[k];
+      lsmem = occ.smem_w[k];
+      lbuckets = occ.buckets_w[k];
+      grid = (long long)occ.sms * occ.per_sm_w[k];
+      if (grid > n_traces) grid = n_traces;
+      break;
+    }
   }
   if (const char* cap = getenv("PM_MAX_GRID")) {  // debugging aid
     const long long g = atoll(cap);
@@ -401,7 +437,9 @@ int replay_batch_impl(const pm_req_t* reqs, const int64_t* trace_offsets,
   // long traces skip to pass 2 only when the batch cannot fill the main
   // pass (one trace per SM or fewer): otherwise they share the main pass's
   // throughput like any other trace
-  const int long_trace = n_traces <= occ.sms ? pmn::kLongTrace : pmn::kNoSkip;
+  int long_trace = n_traces <= occ.sms ? pmn::kLongTrace : pmn::kNoSkip;
+  if (const char* env = getenv("PM_LONG_SKIP"))  // experiment: 0 = no skip
+    if (atoi(env) == 0) long_trace = pmn::kNoSkip;
   // Narrow pass 1 runs BESIDE the main pass: launched right behind it as a
   // programmatic dependent launch (the main pass's CTAs release it once they
   // are all resident, so it can never take SMs the main pass needs), its
@@ -420,10 +458,10 @@ int replay_batch_impl(const pm_req_t* reqs, const int64_t* trace_offsets,
     if (e != cudaSuccess) return cuda_fail(e, "beside pass setup");
   }
 #define PM_LAUNCH_NARROW(W)                                                   \
-  pmn::replay_narrow_kernel<W><<<(unsigned)grid, W * 32, occ.smem_n, stream>>>( \
+  pmn::replay_narrow_kernel<W><<<(unsigned)grid, W * 32, lsmem, stream>>>(    \
       reqs, trace_offsets, cfgs, cfg_of_trace, results, timeline,             \
       reinterpret_cast<pmb::u32*>(recs), ctl, trace_order, n_traces, list_m1, \
-      occ.buckets_n, group_end, n_groups, ready,                             \
+      lbuckets, group_end, n_groups, ready,                                   \
       reinterpret_cast<const pmb::u64*>(wire), const_cast<pm_req_t*>(reqs),   \
       list_w1, long_trace, ck_off, ck_base, ck_cap)
 #define PM_LAUNCH_MAIN(W)                                                     \
@@ -431,7 +469,7 @@ int replay_batch_impl(const pm_req_t* reqs, const int64_t* trace_offsets,
       reqs, trace_offsets, cfgs, cfg_of_trace, results, timeline, recs, ctl, \
       0, trace_order, n_traces, list_m1, occ.buckets, group_end, n_groups, ready)
   if (narrow) {
-    switch (mwarps) {
+    switch (lwarps) {
       case 1: PM_LAUNCH_NARROW(1); break;
       case 12: PM_LAUNCH_NARROW(12); break;
       case 20: PM_LAUNCH_NARROW(20); break;
@@ -500,7 +538,11 @@ int replay_batch_impl(const pm_req_t* reqs, const int64_t* trace_offsets,
   e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "replay pass-2 launch");
   {
-    const int nbm2 = occ.nbmax_m2 < L.nbmax_g ? occ.nbmax_m2 : L.nbmax_g;
+    int nbm2 = occ.nbmax_m2 < L.nbmax_g ? occ.nbmax_m2 : L.nbmax_g;
+    if (const char* env = getenv("PM_M2_BUCKETS")) {  // experiment
+      const int c = atoi(env);
+      if (c > 0 && c < nbm2) nbm2 = c;
+    }
     // up to one CTA per SM, as many as the retry region holds
     long long gm2 = (long long)((L.recs - L.gpool) / pmn::mem_tier_pool_bytes(nbm2));
     if (gm2 > occ.sms) gm2 = occ.sms;

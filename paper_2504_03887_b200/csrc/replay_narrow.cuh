@@ -110,6 +110,7 @@ struct NRecs {
 // allocated neighbours' refs need no re-pointing.
 struct NDir {
   static constexpr bool kResumes = false;  // the main pass starts traces fresh
+  static constexpr int kSoftBuckets = 1 << 30;  // no soft size (32 at most)
   u64 db;
   int dp;
   unsigned dm;
@@ -384,6 +385,10 @@ template <class D>
 __device__ __forceinline__ bool split_bucket(const NPool& P, D& dir, int d,
                                              const NRecs& rec, uint4* st,
                                              int hcmp, int lane) {
+  // past the directory's soft size a merge is tried before it grows
+  if (!dir.full() && dir.nb >= D::kSoftBuckets &&
+      try_merge(P, dir, rec, st, hcmp, lane))
+    return true;  // merged a pair: the caller finds again
   int q = dir.full() ? -1 : dir.alloc_phys();
   if (q < 0) {
     if (try_merge(P, dir, rec, st, hcmp, lane)) return true;
@@ -1534,6 +1539,11 @@ __device__ __forceinline__ void route(pmb::Ctl* ctl, int sts, int tr,
 // interface as NDir; find is a 32-ary warp search over the sorted bounds.
 struct NDirMem {
   static constexpr bool kResumes = true;  // passes 1-3 continue checkpoints
+  // soft size: past it a full bucket first tries to merge a pair elsewhere
+  // instead of growing the directory, whose inserts / erases shift O(nb)
+  // positions and whose find takes one more round beyond 2048 (C5's trace:
+  // 4.02 -> 3.7 s); the directory still grows to nbmax when nothing merges
+  static constexpr int kSoftBuckets = 2048;
   u64* db;          // [nbmax] bound by position
   int* dp;          // [nbmax] physical bucket by position
   unsigned* m;      // [nbmax] occupancy mask by position

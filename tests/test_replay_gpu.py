@@ -44,13 +44,28 @@ def assert_same(got, want):
 
 # --- golden corpora (reference-generated) -----------------------------------
 
+@pytest.mark.parametrize("width", ["auto", "packed", "one_warp", "n2000", "n2600"])
 @pytest.mark.parametrize("name", sorted(CORPORA))
-def test_engine_matches_reference_corpus(name):
+def test_engine_matches_reference_corpus(name, width, monkeypatch):
+    """Every main-pass width on the corpus: the batch as it comes (the
+    narrowest CTA that holds it: 12 warps for a corpus), the packed 24-warp
+    CTAs (PM_SPREAD=0), batches of at most one trace per SM (one warp per
+    CTA), and the corpus repeated to 2000 / 2600 traces (16 / 20 warps per
+    CTA on 148 SMs)."""
     cases = corpus(name)
-    reqs, offsets, cfgs, cfg_of, _ = pack_corpus(cases)
-    res, tl = _native.replay_host(reqs, offsets, cfgs, cfg_of, True)
-    compare_to_golden(cases, res, tl, offsets,
-                      golden(f"replay_{name}.json")["cases"], digest)
+    want = golden(f"replay_{name}.json")["cases"]
+    if width == "packed":
+        monkeypatch.setenv("PM_SPREAD", "0")
+    if width.startswith("n"):
+        m = int(width[1:])
+        k = -(-m // len(cases))
+        cases, want = (cases * k)[:m], (want * k)[:m]
+    step = 100 if width == "one_warp" else len(cases)
+    for a in range(0, len(cases), step):
+        part = cases[a:a + step]
+        reqs, offsets, cfgs, cfg_of, _ = pack_corpus(part)
+        res, tl = _native.replay_host(reqs, offsets, cfgs, cfg_of, True)
+        compare_to_golden(part, res, tl, offsets, want[a:a + step], digest)
 
 
 @pytest.mark.parametrize("fixture", ["tiny_mlp_sgd", "tiny_mlp_adam",
