@@ -23,6 +23,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--c3", type=int, default=42)
     ap.add_argument("--check", action="store_true")
+    ap.add_argument("--reps", type=int, default=3)
     args = ap.parse_args()
     import torch
     import __graft_entry__
@@ -39,17 +40,23 @@ def main():
     b = DeviceBatch(big, boffs, rec, cfg_of)
     b.launch()
     torch.cuda.synchronize()
-    times = []
-    for _ in range(3):
+    times, dev_ms = [], []
+    for _ in range(args.reps):
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
         t0 = time.perf_counter()
+        e0.record()
         b.launch()
+        e1.record()
         torch.cuda.synchronize()
         times.append(time.perf_counter() - t0)
+        dev_ms.append(round(e0.elapsed_time(e1), 2))
     res = b.results()
     ev = int(res["n_events_replayed"].sum())
     line = {"workload": "C4", "traces": len(offs) - 1, "configs": len(cfgs),
             "replays": len(boffs) - 1, "requests": ev, "seconds": min(times),
             "events_per_s": ev / min(times),
+            "device_ms": dev_ms, "wall_ms": [round(t * 1e3, 2) for t in times],
             "statuses": sorted(set(res["status"].tolist())),
             "retry_passes": b.tier_counts(),
             "max_free_blocks": int(res["max_free_blocks"].max()),
