@@ -3,7 +3,7 @@ profiles/replay_ncu_summary.json (read by bench.py for `traffic` and the
 issue bound).
 
     ncu -i prof.ncu-rep --page raw --csv > raw.csv
-    python tools/ncu_summary.py raw.csv <events in the profiled launch> "<capture command>"
+    python tools/ncu_summary.py raw.csv <events in the profiled launch> "<capture command>" [out.json]
 """
 
 import csv
@@ -52,7 +52,8 @@ def main():
         "stall_pct": {s: round(100 * v / tot, 1) for s, v in
                       sorted(samples.items(), key=lambda x: -x[1]) if v / tot > 0.005},
     }
-    Path("profiles/replay_ncu_summary.json").write_text(json.dumps(out, indent=1) + "\n")
+    dest = sys.argv[4] if len(sys.argv) > 4 else "profiles/replay_ncu_summary.json"
+    Path(dest).write_text(json.dumps(out, indent=1) + "\n")
     print(json.dumps(out, indent=1))
 
 
