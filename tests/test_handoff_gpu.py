@@ -99,3 +99,25 @@ def test_handed_on_twice_and_validated():
     res, tlv = _native.replay_host(reqs[:k], offs[:3], cfg, None, True, validate=True)
     assert (res == want[:2]).all()
     assert (tlv == tl_ref[:2 * k]).all()
+
+
+def test_c5_size_trace_vs_oracle():
+    """BASELINE's C5 at its stated size: one 10^7-event trace (357,200 leaf
+    layers, 2 iterations -> 4.29 M requests, 45 k free blocks at peak) --
+    main pass, pass 1, pass 1b, then pass 2, whose directory is kept under
+    its soft size by merging -- equals the oracle, full timeline included."""
+    import paper_2504_03887_b200 as api
+    from paper_2504_03887_b200 import synth_events
+    b = synth_events.generate(357_200, 2)
+    assert len(b.start) > 10_000_000
+    reqs = api.build_sequence(api.analyze(b), 2).packed
+    offs = np.array([0, len(reqs)], dtype=np.int64)
+    cfg = cfg_record(AllocatorConfig())
+    d = DeviceBatch(reqs, offs, cfg, timeline=True)
+    d.launch()
+    got, tl = d.results(), d.timeline()
+    want, tl_ref = oracle.replay_batch(reqs, offs, cfg, timeline=True)
+    assert (got == want).all()
+    assert (tl == tl_ref[:len(tl)]).all()
+    assert int(want["max_free_blocks"][0]) > 40_000
+    assert d.tier_counts()[2] == 1  # finished in pass 2
