@@ -1,6 +1,8 @@
 """Small replay batches for compute-sanitizer (racecheck / memcheck):
 C3 traces through the main pass, corpus traces with capacities and split
-thresholds, hole traces through the retry passes, wire words zero-copy.
+thresholds, hole traces through the retry passes, wire words zero-copy;
+batches of at most one trace per SM run the one-warp main-pass CTA, the
+300-trace batch the 12-warp one (PM_SPREAD=0: every batch in 24-warp CTAs).
 
     compute-sanitizer --tool racecheck python tools/sanitize_replay.py
 """
@@ -39,6 +41,11 @@ def main():
     words = _native.wire_pack(reqs, offs)
     got, _ = _native.replay_host_wire(words, offs, cfg, None, False)
     want, _ = oracle.replay_batch(reqs, offs, cfg)
+    assert (got == want).all()
+    # a batch of more than one trace per SM: the 12-warp main-pass CTA
+    r, o, c, f, _ = pack_corpus(corpus("corpus_seed1000")[:300])
+    got, _ = _native.replay_host(r, o, c, f, True)
+    want, _ = oracle.replay_batch(r, o, c, f)
     assert (got == want).all()
     print("sanitize batches ok")
 
