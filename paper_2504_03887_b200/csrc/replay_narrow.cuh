@@ -110,7 +110,9 @@ struct NRecs {
 // allocated neighbours' refs need no re-pointing.
 struct NDir {
   static constexpr bool kResumes = false;  // the main pass starts traces fresh
-  static constexpr int kSoftBuckets = 1 << 30;  // no soft size (32 at most)
+  // no soft size (32 positions at most)
+  __device__ __forceinline__ bool soft_due() const { return false; }
+  __device__ __forceinline__ void soft_failed() {}
   u64 db;
   int dp;
   unsigned dm;
@@ -386,9 +388,10 @@ __device__ __forceinline__ bool split_bucket(const NPool& P, D& dir, int d,
                                              const NRecs& rec, uint4* st,
                                              int hcmp, int lane) {
   // past the directory's soft size a merge is tried before it grows
-  if (!dir.full() && dir.nb >= D::kSoftBuckets &&
-      try_merge(P, dir, rec, st, hcmp, lane))
-    return true;  // merged a pair: the caller finds again
+  if (!dir.full() && dir.soft_due()) {
+    if (try_merge(P, dir, rec, st, hcmp, lane)) return true;  // the caller finds again
+    dir.soft_failed();
+  }
   int q = dir.full() ? -1 : dir.alloc_phys();
   if (q < 0) {
     if (try_merge(P, dir, rec, st, hcmp, lane)) return true;
@@ -1543,7 +1546,12 @@ struct NDirMem {
   // instead of growing the directory, whose inserts / erases shift O(nb)
   // positions and whose find takes one more round beyond 2048 (C5's trace:
   // 4.02 -> 3.7 s); the directory still grows to nbmax when nothing merges
+  // (after a failed attempt the next one waits for 64 more positions, so a
+  // dense directory is not rescanned on every split)
   static constexpr int kSoftBuckets = 2048;
+  int soft_at;
+  __device__ __forceinline__ bool soft_due() const { return nb >= soft_at; }
+  __device__ __forceinline__ void soft_failed() { soft_at = nb + 64; }
   u64* db;          // [nbmax] bound by position
   int* dp;          // [nbmax] physical bucket by position
   unsigned* m;      // [nbmax] occupancy mask by position
@@ -1561,6 +1569,7 @@ struct NDirMem {
   __device__ __forceinline__ void init(int lane_) {
     lane = lane_;
     nb = 0;
+    soft_at = kSoftBuckets;
     sb = sb2 = ~0ull;
     __syncwarp();
     for (int i = lane; i < nbmax; i += 32) pstack[i] = nbmax - 1 - i;
@@ -1686,6 +1695,7 @@ struct NDirMem {
   }
   __device__ __forceinline__ void release_all() {
     nb = 0;
+    soft_at = kSoftBuckets;
     sb = sb2 = ~0ull;
   }
   __device__ __forceinline__ void release_victim_token() {}
