@@ -24,6 +24,7 @@ def main():
     ap.add_argument("--c3", type=int, default=42)
     ap.add_argument("--check", action="store_true")
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--lib", default=None, help="an alternative build of the engine")
     args = ap.parse_args()
     import torch
     import __graft_entry__
@@ -31,6 +32,9 @@ def main():
     from c4_cases import c4_batch, c4_configs
     from paper_2504_03887_b200 import synth
     from paper_2504_03887_b200.engine import DeviceBatch
+    if args.lib:
+        from paper_2504_03887_b200 import _native
+        _native._lib = _native.load_library(args.lib)
     z = np.load(ROOT / "tests" / "golden" / "c2_sequences.npz")
     r3, o3 = synth.generate(args.c3, first=9000)
     reqs = np.concatenate([z["reqs"], r3])
