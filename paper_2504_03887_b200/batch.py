@@ -33,7 +33,6 @@ from .orchestration import plan_sequence
 from .trace import NONE, EventCategory, TraceBundle
 
 
-
 @dataclass
 class _Trace:
     cols: dict

@@ -717,9 +717,22 @@ void adopt_part(Cols& A, Cols&& B) {
 
 // Parallel strict UTF-8 check: the text is cut at T points moved forward
 // to a byte that starts a sequence (UTF-8 resynchronises there).
+// parses running at once in this process: a parse's threads share the cores
+// with the others (a thread pool of parse_trace calls would otherwise start
+// cores x pool threads)
+std::atomic<int> g_active_parses{0};
+
+unsigned share_of_cores() {
+  unsigned T = std::thread::hardware_concurrency();
+  const char* env = getenv("PM_INGEST_SHARE");  // experiment: 0 = every parse uses all cores
+  const int active = g_active_parses.load();
+  if (!(env && atoi(env) == 0) && active > 1) T = std::max(1u, T / (unsigned)active);
+  return T;
+}
+
 bool valid_utf8_parallel(const unsigned char* p, const unsigned char* end) {
   const size_t len = (size_t)(end - p);
-  unsigned T = std::thread::hardware_concurrency();
+  unsigned T = share_of_cores();
   if (T > 16) T = 16;
   if (len / T < (4u << 20)) T = (unsigned)(len >> 22);
   if (T < 2) return valid_utf8(p, end);
@@ -750,7 +763,7 @@ bool valid_utf8_parallel(const unsigned char* p, const unsigned char* end) {
 void parse_records(Parser& P, Cols& C, bool strict) {
   const char* begin = P.p;
   const size_t len = (size_t)(P.end - begin);
-  unsigned T = std::thread::hardware_concurrency();
+  unsigned T = share_of_cores();
   if (T > 16) T = 16;
   if (len / T < (1u << 20)) T = (unsigned)(len >> 20);
   // records are laid out like the first one: a newline, its indentation,
@@ -846,6 +859,10 @@ const char* pm_ingest_last_error(void) { return g_err.c_str(); }
 // PM_INGEST_UNSUPPORTED (5: use the Python reader) or PM_INGEST_EMPTY (7).
 int pm_ingest_json(const char* text, int64_t len, int strict, void** handle) {
   *handle = nullptr;
+  g_active_parses.fetch_add(1);
+  struct Leave {
+    ~Leave() { g_active_parses.fetch_sub(1); }
+  } leave;
   if (!valid_utf8_parallel(reinterpret_cast<const unsigned char*>(text),
                            reinterpret_cast<const unsigned char*>(text) + len)) {
     g_err = "input is not valid UTF-8";
