@@ -45,6 +45,8 @@ def main():
     out["estimate_many_ms"] = timed(lambda: est.estimate_many(bundles))
     out["digests_8_threads_ms"] = timed(lambda: list(ThreadPoolExecutor(8).map(
         lambda b: est._digest(b, 0, 0), bundles)))
+    out["digests_16_threads_ms"] = timed(lambda: list(ThreadPoolExecutor(16).map(
+        lambda b: est._digest(b, 0, 0), bundles)))
     out["digest_one_ms"] = timed(lambda: est._digest(bundles[0], 0, 0))
     out["build_sequences_ms"] = timed(lambda: build_sequences(bundles, iterations=2))
     seqs = build_sequences(bundles, iterations=2)
