@@ -148,3 +148,10 @@ def test_estimate_many_digest_error_after_replay(monkeypatch):
     with pytest.raises(ValueError, match="digest"):
         PeakMemoryEstimator().estimate(Bundle())
     assert calls == ["build", "replay"]
+
+
+def test_estimate_many_of_no_bundles_is_empty():
+    # parameters are still validated; nothing reaches the device
+    assert PeakMemoryEstimator().estimate_many([]) == []
+    with pytest.raises(ValueError):
+        PeakMemoryEstimator(iterations=0).estimate_many([])
