@@ -39,8 +39,13 @@ def no_injection():
     lib.pm_validate_inject(0, 0)
 
 
+@pytest.mark.parametrize("packed", [False, True])
 @pytest.mark.parametrize("name", ["corpus_seed1000", "corpus_seed2024"])
-def test_reference_corpora_replay_clean(name):
+def test_reference_corpora_replay_clean(name, packed, monkeypatch):
+    """In the 12-warp CTAs the batch size selects, and packed into 24-warp
+    CTAs (PM_SPREAD=0)."""
+    if packed:
+        monkeypatch.setenv("PM_SPREAD", "0")
     cases = corpus(name)
     reqs, offsets, cfgs, cfg_of, _ = pack_corpus(cases)
     res, tl = _native.replay_host(reqs, offsets, cfgs, cfg_of, True, validate=True)
