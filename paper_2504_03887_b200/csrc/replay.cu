@@ -434,12 +434,15 @@ int replay_batch_impl(const pm_req_t* reqs, const int64_t* trace_offsets,
     const long long g = atoll(cap);
     if (g > 0 && g < grid) grid = g;
   }
-  // long traces skip to pass 2 only when the batch cannot fill the main
-  // pass (one trace per SM or fewer): otherwise they share the main pass's
-  // throughput like any other trace
-  int long_trace = n_traces <= occ.sms ? pmn::kLongTrace : pmn::kNoSkip;
-  if (const char* env = getenv("PM_LONG_SKIP"))  // experiment: 0 = no skip
-    if (atoi(env) == 0) long_trace = pmn::kNoSkip;
+  // Long traces start in the main pass like any other: a trace that outgrows
+  // a pass continues in the next from its checkpoint, so nothing is replayed
+  // twice (the round-1 rule sent traces of >= 2^20 requests in batches of at
+  // most one per SM straight to pass 2, when a hand-off restarted at request
+  // 0; with checkpoints C5's lone trace is 3.68 s that way, 3.53 s through
+  // the passes).  PM_LONG_SKIP=1 restores the skip.
+  int long_trace = pmn::kNoSkip;
+  if (const char* env = getenv("PM_LONG_SKIP"))
+    if (atoi(env) != 0 && n_traces <= occ.sms) long_trace = pmn::kLongTrace;
   // Narrow pass 1 runs BESIDE the main pass: launched right behind it as a
   // programmatic dependent launch (the main pass's CTAs release it once they
   // are all resident, so it can never take SMs the main pass needs), its

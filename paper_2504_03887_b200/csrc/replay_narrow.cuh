@@ -1515,8 +1515,9 @@ __device__ __forceinline__ NStage carve_stage(char* wst) {
 // continues where it stopped.
 // A capacity overflow moves a trace to the next capacity tier; an encoding
 // limit sends it to the first wide tier.
-// requests: a trace this long goes straight to pass 2 when the batch is too
-// small to fill the main pass anyway (the host passes kNoSkip otherwise)
+// requests: with PM_LONG_SKIP=1 a trace this long goes straight to pass 2
+// when the batch is too small to fill the main pass anyway (the host passes
+// kNoSkip otherwise, the default)
 constexpr int kLongTrace = 1 << 20;
 constexpr int kNoSkip = 0x7FFFFFFF;
 constexpr int kTierMemSmem = 1;

@@ -12,7 +12,8 @@ import json
 import sys
 
 SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9,
-         "nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3, "second": 1.0}
+         "nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3, "second": 1.0,
+         "ns": 1e-9, "us": 1e-6, "ms": 1e-3, "s": 1.0}
 STALLS = ["wait", "short_scoreboard", "long_scoreboard", "branch_resolving",
           "barrier", "membar", "lg_throttle", "mio_throttle", "math_pipe_throttle",
           "no_instructions", "selected", "not_selected", "dispatch_stall", "misc",
