@@ -460,6 +460,19 @@ int replay_batch_impl(const pm_req_t* reqs, const int64_t* trace_offsets,
     e = cudaMemsetAsync(list_m1, 0xFF, 4 * nt, stream);  // slots start at -1
     if (e != cudaSuccess) return cuda_fail(e, "beside pass setup");
   }
+  // A packed batch of one wave with a short tail: its long traces fill the
+  // first CTAs warp-major and the tail whole CTAs, which free their SMs early
+  // for the pass-1 grid beside (pmn::pos_prep_kernel; PM_TAIL_CTAS=0: the
+  // atomic counter throughout).
+  if (narrow && lwarps >= 24 && (long long)n_traces <= grid * lwarps) {
+    const char* env = getenv("PM_TAIL_CTAS");
+    if (!(env && atoi(env) == 0)) {
+      pmn::pos_prep_kernel<<<1, 1024, 0, stream>>>(trace_offsets, trace_order, n_traces,
+                                                   lwarps, (int)grid, ctl);
+      e = cudaGetLastError();
+      if (e != cudaSuccess) return cuda_fail(e, "first-wave split");
+    }
+  }
 #define PM_LAUNCH_NARROW(W)                                                   \
   pmn::replay_narrow_kernel<W><<<(unsigned)grid, W * 32, lsmem, stream>>>(    \
       reqs, trace_offsets, cfgs, cfg_of_trace, results, timeline,             \

@@ -1172,7 +1172,8 @@ struct Ctl {
   unsigned long long ck_used;  // checkpoint region bump counter (narrow passes)
   unsigned main_exited;        // main-pass CTAs finished
   unsigned main_done;          // 1 once every main-pass CTA has finished
-  unsigned pad[44];
+  int pos_ctas;  // packed main pass: first wave by position (0: counter)
+  unsigned pad[43];
 };
 
 // Shared-memory layout of the main kernel (per CTA): the bucket pool

@@ -1728,6 +1728,42 @@ __host__ __device__ __forceinline__ size_t smem_cta_bytes(int buckets,
          (size_t)((buckets + 31) / 32) * 4 + 12;
 }
 
+// First-wave split of a packed one-wave batch (see replay_narrow_kernel):
+// traces longer than a quarter of the longest are "long"; when they fill
+// fewer CTAs than the grid, ctl->pos_ctas = the CTAs they fill (else 0, the
+// counter).  One block; the batch is at most one wave (a few thousand).
+__global__ void __launch_bounds__(1024)
+    pos_prep_kernel(const int64_t* __restrict__ offs,
+                    const int32_t* __restrict__ list, int n_traces, int warps,
+                    int grid, pmb::Ctl* ctl) {
+  __shared__ long long s_max;
+  __shared__ int s_long;
+  if (threadIdx.x == 0) {
+    s_max = 0;
+    s_long = 0;
+  }
+  __syncthreads();
+  long long mx = 0;
+  for (int i = threadIdx.x; i < n_traces; i += blockDim.x) {
+    const int tr = list ? list[i] : i;
+    mx = max(mx, (long long)(offs[tr + 1] - offs[tr]));
+  }
+  atomicMax(&s_max, mx);
+  __syncthreads();
+  const long long thr = s_max / 4;
+  int cnt = 0;
+  for (int i = threadIdx.x; i < n_traces; i += blockDim.x) {
+    const int tr = list ? list[i] : i;
+    cnt += (offs[tr + 1] - offs[tr]) > thr;
+  }
+  atomicAdd(&s_long, cnt);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int g_long = (s_long + warps - 1) / warps;
+    ctl->pos_ctas = g_long < grid ? g_long : 0;
+  }
+}
+
 // Main pass: persistent warps pull traces (longest first) from a global
 // counter; the CTA's warps share one shared-memory bucket pool.
 template <int WARPS>
@@ -1780,26 +1816,31 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
   dir.cta_used = used;
   dir.cta_words = words;
   dir.cta_buckets = buckets;
-  // Batches under a wave (the narrow widths, 1-20 warps per CTA: a small
-  // sweep, a rank's shard at 4-8 GPUs) start by position, warp-major: SM c's
-  // warps take positions c, c + grid, c + 2 grid, ... of the longest-first
-  // order, so every SM holds one trace of each length class and no SM's
-  // warps are all long ones (the atomic counter hands the longest traces to
-  // whichever CTAs start first, often the same SMs): 1250 C3 traces 111.6 ->
-  // 96.2 ms.  The packed width keeps the counter from the start: a C4 wave
-  // is faster when some SMs run short traces only and free up early for
-  // the beside pass (159 vs 126-157 ms measured).  Positions [0, grid x
-  // WARPS) are each taken once; the counter continues after them.
+  // First wave by position.  Batches under a wave (the narrow widths, 1-20
+  // warps per CTA: a small sweep, a rank's shard at 4-8 GPUs) start
+  // warp-major: SM c's warps take positions c, c + grid, c + 2 grid, ... of
+  // the longest-first order, so every SM holds one trace of each length
+  // class and no SM's warps are all long ones (the atomic counter hands the
+  // longest traces to whichever CTAs start first, often the same SMs):
+  // 1250 C3 traces 111.6 -> 97.7 ms.  A packed batch of one wave with a
+  // short tail (C4: 2898 C3-length replays, 552 GPT-2-length ones) gets
+  // ctl->pos_ctas = the CTAs its long traces fill (pos_prep_kernel): those
+  // CTAs take the long positions warp-major, the remaining CTAs the short
+  // tail CTA by CTA, so whole SMs free up early for the pass-1 grid beside
+  // (the counter left that to launch timing: C4 126 or 157 ms).  Positions
+  // [0, grid x WARPS) are each taken once; the counter continues after them.
   constexpr bool kByPosition = WARPS < 24;
   const unsigned wave = gridDim.x * WARPS;
-  bool first = kByPosition;
+  const unsigned pc = kByPosition ? gridDim.x : (unsigned)ctl->pos_ctas;
+  bool first = pc > 0;
   for (;;) {
     unsigned t = 0;
     if (first) {
-      t = (unsigned)wib * gridDim.x + blockIdx.x;
+      const unsigned c = blockIdx.x;
+      t = c < pc ? (unsigned)wib * pc + c : pc * WARPS + (c - pc) * WARPS + wib;
       first = false;
     } else {
-      if (lane == 0) t = (kByPosition ? wave : 0u) + atomicAdd(&ctl->work[0], 1u);
+      if (lane == 0) t = (pc > 0 ? wave : 0u) + atomicAdd(&ctl->work[0], 1u);
       t = __shfl_sync(kFull, t, 0);
     }
     if (t >= (unsigned)n_traces) break;
