@@ -467,8 +467,12 @@ int replay_batch_impl(const pm_req_t* reqs, const int64_t* trace_offsets,
   if (narrow && lwarps >= 24 && (long long)n_traces <= grid * lwarps) {
     const char* env = getenv("PM_TAIL_CTAS");
     if (!(env && atoi(env) == 0)) {
+      // long traces per long CTA (PM_TAIL_PER_CTA, experiment)
+      int per_cta = lwarps;
+      if (const char* pe = getenv("PM_TAIL_PER_CTA"))
+        if (atoi(pe) > 0 && atoi(pe) <= lwarps) per_cta = atoi(pe);
       pmn::pos_prep_kernel<<<1, 1024, 0, stream>>>(trace_offsets, trace_order, n_traces,
-                                                   lwarps, (int)grid, ctl);
+                                                   per_cta, (int)grid, ctl);
       e = cudaGetLastError();
       if (e != cudaSuccess) return cuda_fail(e, "first-wave split");
     }

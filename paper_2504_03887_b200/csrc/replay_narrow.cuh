@@ -1734,7 +1734,7 @@ __host__ __device__ __forceinline__ size_t smem_cta_bytes(int buckets,
 // counter).  One block; the batch is at most one wave (a few thousand).
 __global__ void __launch_bounds__(1024)
     pos_prep_kernel(const int64_t* __restrict__ offs,
-                    const int32_t* __restrict__ list, int n_traces, int warps,
+                    const int32_t* __restrict__ list, int n_traces, int per_cta,
                     int grid, pmb::Ctl* ctl) {
   __shared__ long long s_max;
   __shared__ int s_long;
@@ -1759,7 +1759,7 @@ __global__ void __launch_bounds__(1024)
   atomicAdd(&s_long, cnt);
   __syncthreads();
   if (threadIdx.x == 0) {
-    const int g_long = (s_long + warps - 1) / warps;
+    const int g_long = (s_long + per_cta - 1) / per_cta;
     ctl->pos_ctas = g_long < grid ? g_long : 0;
   }
 }
