@@ -10,5 +10,5 @@ timeout 600 python bench.py --impl reference --steps 20 --warmup 3 > gpurun_out/
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
   --log-file gpurun_out/${TAG}_launches.csv python bench.py --steps 2 --warmup 1 --no-other-configs \
   > /dev/null 2>&1; echo "launches rc=$?"
-bash tools/gpu/r2_c5skip.sh > gpurun_out/${TAG}_c5skip.log 2>&1; echo "c5 rc=$?"
-bash tools/gpu/r2_pipe_ncu.sh ${TAG} > gpurun_out/${TAG}_pipe.log 2>&1; echo "pipe ncu rc=$?"
+
+
