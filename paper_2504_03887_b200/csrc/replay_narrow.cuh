@@ -1402,16 +1402,17 @@ __device__ __forceinline__ void replay_trace(
         }
       }
 #endif
-      if (sts != PM_OK) {
-        status = sts;
-        stop = cbase + j;
-        break;
-      }
-      if (tl != nullptr && lane == j)
-        tl[cbase + j] =
-            make_longlong2(c.reserved, c.allocated);
-      __syncwarp();
-      if (handoff) {
+      // one test on the common path: an error stops before the request, a
+      // hand-off after it (its timeline entry is written first)
+      if (sts != PM_OK || handoff) {
+        if (sts != PM_OK) {
+          status = sts;
+          stop = cbase + j;
+          break;
+        }
+        if (tl != nullptr && lane == j)
+          tl[cbase + j] = make_longlong2(c.reserved, c.allocated);
+        __syncwarp();
         // the request is complete; continue at the next one in the next pass
         status = PM_POOL_OVERFLOW;
         stop = cbase + j + 1;
@@ -1425,6 +1426,9 @@ __device__ __forceinline__ void replay_trace(
         }
         break;  // the checkpoint is written after the chunk loop
       }
+      if (tl != nullptr && lane == j)
+        tl[cbase + j] = make_longlong2(c.reserved, c.allocated);
+      __syncwarp();
     }
     __syncwarp();
     sg.g += 1;
