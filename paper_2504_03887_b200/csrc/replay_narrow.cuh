@@ -1229,10 +1229,10 @@ __device__ __forceinline__ void replay_trace(
         bool split_out = false;
         u32 out_a = 0, out_s = 0, out_L = kNone, out_R = kNone;
         if (is_alloc) {
-          if (rj.y != 0) {
-            sts = PM_DUPLICATE_HANDLE;
-          } else if (pre != PM_OK) {
-            sts = pre;  // zero size / outside the encoding
+          // one test for the rare errors: a duplicate handle first, then the
+          // prologue's zero size / encoding limit
+          if (rj.y != 0 || pre != PM_OK) {
+            sts = rj.y != 0 ? PM_DUPLICATE_HANDLE : pre;
           } else {
             const u32 ru = ev.x;
             const u32 split_lim = k_split;
@@ -1302,10 +1302,8 @@ __device__ __forceinline__ void replay_trace(
           }
         } else {
           // free (allocator.py:294-320): double free before unknown handle
-          if (rj.y == kFreedU) {
-            sts = PM_DOUBLE_FREE;
-          } else if (rj.y == 0) {
-            sts = PM_UNKNOWN_HANDLE;
+          if (rj.y - 1u >= kFreedU - 1u) {  // rj.y == 0 or rj.y == kFreedU
+            sts = rj.y == 0 ? PM_UNKNOWN_HANDLE : PM_DOUBLE_FREE;
           } else {
             const u32 A = rj.x, S = rj.y, L = rj.z, R = rj.w;
             c.allocated -= (long long)S << s;
