@@ -110,6 +110,8 @@ struct NRecs {
 // allocated neighbours' refs need no re-pointing.
 struct NDir {
   static constexpr bool kResumes = false;  // the main pass starts traces fresh
+  // find() on an empty directory gives -1, whose shuffled mask is 0
+  static constexpr bool kEmptyFindSafe = true;
   // no soft size (32 positions at most)
   __device__ __forceinline__ bool soft_due() const { return false; }
   __device__ __forceinline__ void soft_failed() {}
@@ -445,33 +447,51 @@ template <class D>
 __device__ __forceinline__ int pool_insert(const NPool& P, D& dir, NCtx& c,
                                            u64 ka, u64 links, const NRecs& rec,
                                            uint4* st, int hcmp, int lane) {
-  bool room = true;
-  if (dir.nb == 0) {
-    const int q = dir.alloc_phys_wait();
-    if (q < 0)
-      room = false;
-    else
-      dir.insert(0, 0ull, q, 0u);
-  }
+  // common case in one test: a directory with a bucket of room for ka
+  // (the register directory's find on an empty directory gives -1 with a
+  // zero mask, so the empty case folds into the same rare branch)
   int d = 0;
   unsigned m = 0;
-  if (room) {
+  bool rare;
+  if constexpr (D::kEmptyFindSafe) {
     d = dir.find(ka);
     m = dir.mask(d);
-    while (m == kFull) {
-      // a full directory whose buckets are >= 3/4 occupied would thrash
-      // (merge a pair, split, merge ...) on every insert: hand the trace to
-      // the next pass, which has room, instead
-      if ((dir.full() && c.F >= 24 * dir.capacity()) ||
-          !split_bucket(P, dir, d, rec, st, hcmp, lane)) {
-        room = false;
-        break;
-      }
+    rare = dir.nb == 0 || m == kFull;
+  } else {
+    rare = dir.nb == 0;
+    if (!rare) {
       d = dir.find(ka);
       m = dir.mask(d);
+      rare = m == kFull;
     }
   }
-  if (!room) return stash_entry(c, ka, links);
+  if (rare) {
+    bool room = true;
+    if (dir.nb == 0) {
+      const int q = dir.alloc_phys_wait();
+      if (q < 0)
+        room = false;
+      else
+        dir.insert(0, 0ull, q, 0u);
+    }
+    if (room) {
+      d = dir.find(ka);
+      m = dir.mask(d);
+      while (m == kFull) {
+        // a full directory whose buckets are >= 3/4 occupied would thrash
+        // (merge a pair, split, merge ...) on every insert: hand the trace to
+        // the next pass, which has room, instead
+        if ((dir.full() && c.F >= 24 * dir.capacity()) ||
+            !split_bucket(P, dir, d, rec, st, hcmp, lane)) {
+          room = false;
+          break;
+        }
+        d = dir.find(ka);
+        m = dir.mask(d);
+      }
+    }
+    if (!room) return stash_entry(c, ka, links);
+  }
   const int slot = __ffs(~m) - 1;
   const int id = dir.phys(d) * kBucket + slot;
   PM_STAT(5);
@@ -1545,6 +1565,7 @@ __device__ __forceinline__ void route(pmb::Ctl* ctl, int sts, int tr,
 // interface as NDir; find is a 32-ary warp search over the sorted bounds.
 struct NDirMem {
   static constexpr bool kResumes = true;  // passes 1-3 continue checkpoints
+  static constexpr bool kEmptyFindSafe = false;  // positions index memory
   // soft size: past it a full bucket first tries to merge a pair elsewhere
   // instead of growing the directory, whose inserts / erases shift O(nb)
   // positions and whose find takes one more round beyond 2048 (C5's trace:
